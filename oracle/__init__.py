@@ -211,6 +211,19 @@ def search(Q, P, Cr, list_off, list_ids, codes, n_o, rho, X, k, nprobe, M, seed,
     return ids, dists
 
 
+def rerank(Q, X, cand, k, id_offset=0):
+    Q = _c(Q, np.float32)
+    X = _c(X, np.float32)
+    cand = _c(cand, np.int64)
+    nq, D = Q.shape
+    M = cand.shape[1]
+    ids = np.empty((nq, k), np.int64)
+    d = np.empty((nq, k), np.float32)
+    lib().oracle_rerank(_p(Q), ctypes.c_int64(nq), ctypes.c_int(D), _p(X), ctypes.c_int64(id_offset), _p(cand),
+                        ctypes.c_int(M), ctypes.c_int(k), _p(ids), _p(d))
+    return ids, d
+
+
 def merge_topk(in_ids, in_d):
     in_ids = _c(in_ids, np.int64)
     in_d = _c(in_d, np.float32)

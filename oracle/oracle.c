@@ -433,6 +433,30 @@ int oracle_search(const float* Q, int64_t nq, int D, const float* P, const float
     return 0;
 }
 
+/* Fine ranking of a given candidate set. */
+void oracle_rerank(const float* Q, int64_t nq, int D, const float* X, int64_t id_offset,
+                   const int64_t* cand, int M, int k, int64_t* ids, float* dists) {
+    dkey_t* fk = (dkey_t*)malloc(sizeof(dkey_t) * (M > 0 ? M : 1));
+    for (int64_t qi = 0; qi < nq; ++qi) {
+        const float* q = Q + (size_t)qi * D;
+        int m = 0;
+        for (int c = 0; c < M; ++c) {
+            int64_t id = cand[(size_t)qi * M + c];
+            if (id < 0) continue;
+            const float* x = X + (size_t)(id - id_offset) * D;
+            double s = 0.0;
+            for (int d = 0; d < D; ++d) { double t = (double)q[d] - (double)x[d]; s += t * t; }
+            fk[m].d = s; fk[m].id = id; ++m;
+        }
+        qsort(fk, m, sizeof(dkey_t), cmp_dkey);
+        for (int i = 0; i < k; ++i) {
+            ids[(size_t)qi * k + i] = (i < m) ? fk[i].id : -1;
+            dists[(size_t)qi * k + i] = (i < m) ? (float)fk[i].d : INFINITY;
+        }
+    }
+    free(fk);
+}
+
 /* Global top-k over the union of per-shard top-k lists (R#20). */
 void oracle_merge_topk(const int64_t* in_ids, const float* in_d, int G, int64_t nq, int k,
                        int64_t* out_ids, float* out_d) {

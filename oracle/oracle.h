@@ -124,6 +124,12 @@ int oracle_search(const float* Q, int64_t nq, int D, const float* P, const float
                   int64_t* ids, float* dists, int32_t* probes_out, int64_t* topm_ids,
                   double* topm_est);
 
+/* Fine ranking of given candidates (O-S6): exact squared L2 in fp64
+ * between q and the raw vectors X[cand - id_offset] (cand = -1 skipped),
+ * top-k by (d, id), padded (-1, +inf).  cand [nq x M] -> ids/dists [nq x k]. */
+void oracle_rerank(const float* Q, int64_t nq, int D, const float* X, int64_t id_offset,
+                   const int64_t* cand, int M, int k, int64_t* ids, float* dists);
+
 /* Merge G per-shard top-k lists into the global top-k by (d, id) (P:L405-407,
  * NS "merges top-k"; R#20).  in_* [G x nq x k] -> out_* [nq x k]. */
 void oracle_merge_topk(const int64_t* in_ids, const float* in_d, int G, int64_t nq, int k,

@@ -1,0 +1,45 @@
+// index.cuh -- the in-HBM layout of an IVF-RaBitQ index.
+//
+//   list j holds the vectors assigned to centroid j, ids
+//   ascending.  Its vectors occupy SLOTS [slot_off[j], slot_off[j] + size_j),
+//   slot_off[j] a multiple of 32.  Codes are stored in blocks of 32 slots,
+//   word-interleaved: word w of slot s is codes[((s / 32) * W + w) * 32 + s % 32],
+//   so a warp reading word w of 32 consecutive slots issues one 128-byte
+//   coalesced load; a 128-slot tile is 128 * W * 4 contiguous bytes.
+//   Pad slots have code 0, factors 0 and row kPadRow.
+#pragma once
+#include <vector>
+
+#include "common.cuh"
+
+struct rabitq_index {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int D = 0, W = 0, nlist = 0;
+    int64_t n = 0, id_offset = 0, nslots = 0, max_list = 0;
+    uint64_t seed = 0;
+
+    float* P = nullptr;            // [D x D] row-major, x' = P^T x
+    float* Cr = nullptr;           // [nlist x D] rotated centroids c'
+    float* cnorm = nullptr;        // [nlist] ||c'||^2
+    int64_t* list_off = nullptr;   // [nlist + 1] list boundaries in list order (rank of vector)
+    int64_t* slot_off = nullptr;   // [nlist + 1] 32-aligned slot starts
+    uint32_t* codes = nullptr;     // [nslots / 32][W][32]
+    float2* fac = nullptr;         // [nslots] {n_o^2, 2 n_o / (rho sqrt(D))}
+    float* g1 = nullptr;           // [nslots] 2 n_o sqrt(1 - rho^2) / (rho sqrt(D - 1))  (bound / (eps0 n_q))
+    float* n_o = nullptr;          // [nslots]
+    float* rho = nullptr;          // [nslots]
+    uint32_t* rows = nullptr;      // [nslots] local row id, kPadRow for pad slots
+    uint32_t* slot_of_row = nullptr;  // [n] inverse of rows (debug capture of bounds)
+    const float* X = nullptr;      // [n x D] fp32 vectors for the exact re-rank (local rows)
+    float* X_owned = nullptr;
+    bool borrowed = false;
+
+    std::vector<int64_t> h_list_off, h_slot_off;
+};
+
+namespace rabitq {
+void build_index(rabitq_index* idx, const float* X, int64_t n, int D, int nlist, uint64_t seed,
+                 const rabitq_build_opts& o);
+void free_index_memory(rabitq_index* idx);
+}  // namespace rabitq

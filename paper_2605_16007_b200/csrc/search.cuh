@@ -1,0 +1,95 @@
+// search.cuh -- argument blocks shared by the scan kernels (popc: search.cu,
+// tcgen05 IMMA: scan_imma.cu) and the host orchestration.
+#pragma once
+#include "index.cuh"
+
+namespace rabitq {
+
+struct ScanArgs {
+    const int32_t* probes;     // [npairs] list of each (q, probe) pair
+    int64_t npairs;
+    int nprobe;
+    const int64_t* item_off;   // [npairs + 1] exclusive scan of 32-slot blocks per pair
+    const int64_t* list_off;
+    const int64_t* slot_off;
+    const uint32_t* codes;
+    const float2* fac;
+    const float* g1;
+    const uint32_t* rows;
+    const uint4* planes;       // [npairs][W] {plane0..3} per 32-dim word
+    const float4* qscal;       // [npairs] {v_l, Delta, ||r_q||^2, S_q}
+    const int8_t* qbar8;       // [npairs][Dpad] int8 quantized query (IMMA path)
+    const float* tau;          // [nq] float threshold
+    const uint64_t* tau64;     // [nq] 64-bit (key, row) threshold (retry)
+    const int* flags;          // [nq] retry flags
+    int* cnt;                  // [nq] survivors appended
+    uint64_t* buf;             // [nq x cap] survivor keys (orderable key << 32 | row)
+    int cap;
+    int D, W;
+    float eps0;
+    int32_t* dump_ip;          // debug: [items x 32] ip per (item, lane)
+    float* dump_est;
+    int64_t dump_cap;
+};
+
+struct RerankArgs {
+    const int* cnt;
+    const uint64_t* buf;
+    int cap, M, k, D;
+    const float* Q;            // [nq x D] unrotated queries (device)
+    const float* X;            // [n x D] vectors (device)
+    int64_t id_offset;
+    int64_t* ids;
+    float* dists;
+    int64_t* topm_ids;
+    float* topm_est;
+    float* topm_bound;
+    int rank_key;
+    float eps0;
+    const uint32_t* slot_of_row;
+    const int64_t* slot_off;
+    int nlist;
+    const int32_t* probes;
+    int nprobe;
+    const float4* qscal;
+    const float* g1;
+};
+
+struct SearchCfg {
+    int scan_path = 0;   // 0 auto, 1 popc, 2 imma
+    int rank_key = 0;
+    float eps0 = 1.9f;
+    int cap = 0;
+    int seed_max = 0;
+};
+
+struct DebugOut {  // device-or-host pointers (cudaMemcpyDefault), all nullable
+    float* qrot = nullptr;
+    int32_t* probes = nullptr;
+    uint8_t* qbar = nullptr;   // written by the quantize kernel directly: must be DEVICE
+    float4* qscal = nullptr;
+    int64_t* topm_ids = nullptr;  // DEVICE
+    float* topm_est = nullptr;    // DEVICE
+    float* topm_bound = nullptr;  // DEVICE
+    float* tau = nullptr;
+    int32_t* survivors = nullptr;
+    int32_t* scan_ip = nullptr;   // DEVICE [scan_dump_cap]
+    float* scan_est = nullptr;    // DEVICE
+    int64_t scan_dump_cap = 0;
+};
+
+struct SearchStats {
+    int retries = 0;
+    int used_imma = 0;
+};
+
+void search_batch(const rabitq_index* idx, const float* Q, int64_t nq, int k, int nprobe, int M,
+                  const SearchCfg& cfg, int64_t qid_base, int64_t* ids, float* dists, const DebugOut& dbg,
+                  cudaStream_t st, SearchStats* stats);
+void scan_dispatch(const ScanArgs& a, const rabitq_index* idx, const SearchCfg& cfg, bool lb, bool dump,
+                   cudaStream_t st, SearchStats* stats);
+void scan_popc_entry(const ScanArgs& a, bool lb, bool retry, bool dump, cudaStream_t st);
+void merge_topk(const int64_t* in_ids, const float* in_d, int G, int64_t nq, int k, int64_t* out_ids,
+                float* out_d, cudaStream_t st);
+
+}  // namespace rabitq

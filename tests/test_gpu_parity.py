@@ -1,0 +1,311 @@
+"""GPU (librabitq via the C ABI) vs the oracle, stage by stage (-m gpu).
+
+Layered parity: L0 build, L1 probe, L2 quantizer (bit-exact under
+injection of the GPU's q'), L3 integer inner products (bit-exact), L4
+estimator (1e-4 n_q n_o + 2^-20 (n_o^2 + n_q^2)), L5 coarse top-M (set equal
+except the tie band), L6 final top-k (oracle re-rank of the GPU's top-M:
+identical except exact-distance ties), end to end, and invariances.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from tests import parity_util as pu
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # the whole module needs a B200
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2605_16007_b200 as rq  # noqa: E402
+
+SEED = 42
+
+
+@pytest.fixture(scope="module")
+def orc():
+    import oracle
+
+    oracle.build()
+    return oracle
+
+
+def make_data(D, N, ncent, nq, kind="iso", seed=7):
+    s = synth.spec(1, D=D, N=N, ncent=ncent, nlist=ncent, nq=nq, kind=kind, data_seed=seed)
+    cen = synth.centres(s, "cpu")
+    X = synth.base_rows(s, 0, N, "cpu", cen=cen)
+    Q = synth.queries(s, "cpu", cen=cen)
+    return X, Q
+
+
+def build(X, nlist, **kw):
+    return rq.Index(X.cuda(), nlist=nlist, seed=SEED, **kw)
+
+
+def debug_search(idx, Q, k, nprobe, M, dump=True, **kw):
+    nq, D = Q.shape
+    dev = "cuda"
+    info = idx.info()
+    dbg = dict(
+        qrot=torch.empty(nq, D, device=dev), probes=torch.empty(nq, nprobe, dtype=torch.int32, device=dev),
+        qbar=torch.empty(nq, nprobe, D, dtype=torch.uint8, device=dev),
+        qscal=torch.empty(nq, nprobe, 4, device=dev), topm_ids=torch.empty(nq, M, dtype=torch.int64, device=dev),
+        topm_est=torch.empty(nq, M, device=dev), topm_bound=torch.empty(nq, M, device=dev),
+        tau=torch.empty(nq, device=dev), survivors=torch.empty(nq, dtype=torch.int32, device=dev),
+        retries=torch.zeros(1, dtype=torch.int32, device=dev),
+    )
+    if dump:
+        cap = nq * nprobe * ((info["max_list"] + 31) // 32) * 32
+        dbg["scan_ip"] = torch.empty(cap, dtype=torch.int32, device=dev)
+        dbg["scan_est"] = torch.empty(cap, device=dev)
+        dbg["scan_dump_cap"] = cap
+    ids, d = idx.search(Q.cuda(), k, nprobe, M, debug=dbg, **kw)
+    torch.cuda.synchronize()
+    out = {k_: (v.cpu().numpy() if torch.is_tensor(v) else v) for k_, v in dbg.items()}
+    return ids.cpu().numpy(), d.cpu().numpy(), out
+
+
+# ----------------------------------------------------------------------------
+@pytest.mark.parametrize("D,N,nlist", [(128, 20000, 64), (96, 12000, 40), (33, 5000, 16)])
+def test_build_parity(orc, D, N, nlist):
+    """L0: the exported lists partition the ids (ascending within a list), every
+    vector sits in its nearest list (fp64, tie band), and the codes/factors
+    equal the oracle's encode of the exported P and centroids."""
+    X, _ = make_data(D, N, nlist, 4)
+    idx = build(X, nlist)
+    ex = idx.export()
+    Xn = X.numpy()
+    P, Cr, off, ids = ex["rotation"], ex["centroids"], ex["list_off"], ex["ids"]
+    assert np.abs(P.astype(np.float64).T @ P.astype(np.float64) - np.eye(D)).max() <= 1e-5  # NS: P^T P = I
+    assert off[0] == 0 and off[-1] == N
+    assert np.array_equal(np.sort(ids), np.arange(N))
+    assign = np.empty(N, np.int32)
+    for j in range(nlist):
+        seg = ids[off[j]:off[j + 1]]
+        assert np.all(np.diff(seg) > 0)
+        assign[seg] = j
+    # nearest list (rotated space, fp64) up to fp32 near-ties
+    Xr = orc.rotate(Xn, P)
+    d = ((Xr[:, None, :] - Cr.astype(np.float64)[None]) ** 2).sum(-1) if N * nlist * D < 2e8 else None
+    if d is not None:
+        best = d.min(1)
+        mine = d[np.arange(N), assign]
+        assert np.all(mine <= best + 1e-4 * np.maximum(best, 1.0))
+    codes, n_o, rho = orc.encode(Xn[ids], P, Cr, assign[ids])
+    # codes identical except bits whose rotated residual is ~0 (fp32 GEMM vs fp64)
+    diff = codes ^ ex["codes"]
+    if diff.any():
+        r = Xr[ids] - Cr[assign[ids]].astype(np.float64)
+        rows, words = np.nonzero(diff)
+        for v, w in zip(rows, words):
+            bits = int(diff[v, w])
+            for b in range(32):
+                if bits >> b & 1:
+                    i = 32 * w + b
+                    assert abs(r[v, i]) <= 1e-5 * n_o[v] + 1e-6, (v, i, r[v, i])
+    assert np.allclose(ex["n_o"], n_o, rtol=1e-5, atol=1e-6)
+    assert np.allclose(ex["rho"], rho, rtol=1e-5, atol=1e-6)
+
+
+def _stage_checks(orc, idx, X, Q, k, nprobe, M, rank_key=0):
+    ex = idx.export()
+    P, Cr, off, lids, codes = ex["rotation"], ex["centroids"], ex["list_off"], ex["ids"], ex["codes"]
+    n_o, rho = ex["n_o"], ex["rho"]
+    Qn, Xn = Q.numpy(), X.numpy()
+    nq, D = Qn.shape
+    ids, d, dbg = debug_search(idx, Q, k, nprobe, M, rank_key=rank_key)
+    qr, probes, qbar, qscal = dbg["qrot"], dbg["probes"], dbg["qbar"], dbg["qscal"]
+    # S1 rotation: q' = P^T q within fp32 GEMM rounding
+    ref_qr = orc.rotate(Qn, P)
+    assert np.abs(qr - ref_qr).max() <= 1e-5 * np.abs(ref_qr).max() + 1e-6
+    # L1 probes (GPU q' injected)
+    pu.check_probe_lists(probes, qr, Cr, nprobe)
+    # L2 quantizer: bit-exact under injection
+    nq2 = np.empty((nq, nprobe))
+    for q in range(nq):
+        for p in range(nprobe):
+            j = int(probes[q, p])
+            qb, vl, dl, sq, n2 = orc.quantize(qr[q], Cr[j], SEED, j, q)
+            assert np.array_equal(qb, qbar[q, p]), (q, p)
+            assert np.float32(vl) == qscal[q, p, 0] and np.float32(dl) == qscal[q, p, 1]
+            assert sq == int(qscal[q, p, 3])
+            assert abs(qscal[q, p, 2] - n2) <= 1e-5 * n2 + 1e-12
+            nq2[q, p] = n2
+    # L3 ip bit-exact + L4 est tolerance, every scanned (pair, slot)
+    pair, lst, pos, valid, nitems = pu.list_pos_of_items(probes.reshape(-1), off)
+    sip, sest = dbg["scan_ip"][: nitems * 32], dbg["scan_est"][: nitems * 32]
+    assert np.all(sip[~valid] == -1)
+    e = np.nonzero(valid)[0]
+    row = off[lst[e]] + pos[e]
+    qb_flat = qbar.reshape(nq * nprobe, D)
+    W = codes.shape[1]
+    checked = 0
+    for t in range(e.size):
+        p_ = pair[e[t]]
+        ipv, pcv = orc.ip(codes[row[t]], qb_flat[p_], D)
+        assert ipv == int(sip[e[t]]), (t, ipv, sip[e[t]])
+        q_, pp = divmod(int(p_), nprobe)
+        est, bd = orc.estimate(ipv, pcv, D, float(n_o[row[t]]), float(rho[row[t]]), float(qscal[q_, pp, 0]),
+                               float(qscal[q_, pp, 1]), int(qscal[q_, pp, 3]), nq2[q_, pp])
+        tol = pu.est_tol(float(n_o[row[t]]), nq2[q_, pp])
+        assert abs(float(sest[e[t]]) - est) <= tol, (t, sest[e[t]], est, tol)
+        checked += 1
+    assert checked == e.size and checked > 0
+    # L5 coarse top-M vs the oracle with the GPU's q' and probes injected
+    oi, od, _, tids, test = orc.search(Qn, P, Cr, off, lids, codes, n_o, rho, Xn, k, nprobe, M, SEED,
+                                       rank_key=rank_key, qr_in=qr, probes_in=probes, debug=True)
+    gt = dbg["topm_ids"]
+    for q in range(nq):
+        a, b = set(gt[q][gt[q] >= 0].tolist()), set(tids[q][tids[q] >= 0].tolist())
+        if a == b:
+            continue
+        mth = test[q][np.isfinite(test[q])].max()
+        band = pu.EST_REL * math.sqrt(nq2[q].max()) * float(n_o.max()) * 4 + 1e-6 * abs(mth)
+        for x in a ^ b:
+            r = int(np.nonzero(lids == x)[0][0])
+            j = int(np.searchsorted(off, r, side="right") - 1)
+            p = int(np.nonzero(probes[q] == j)[0][0])
+            ipv, pcv = orc.ip(codes[r], qbar[q, p], D)
+            est, bd = orc.estimate(ipv, pcv, D, float(n_o[r]), float(rho[r]), float(qscal[q, p, 0]),
+                                   float(qscal[q, p, 1]), int(qscal[q, p, 3]), nq2[q, p])
+            key = est - bd if rank_key == 1 else est
+            assert abs(key - mth) <= band, (q, x, key, mth, band)
+    # L6 final: the oracle's re-rank of the GPU's own top-M
+    ri, rd = orc.rerank(Qn, Xn, gt, k)
+    pu.check_final(ids, d, ri, rd, k)
+    # end to end vs the injected oracle: identical except tie-explained slots
+    return ids, d, oi, od, dbg
+
+
+@pytest.mark.parametrize("D,N,nlist,nq,nprobe,k,M", [
+    (128, 20000, 64, 12, 8, 10, 100),     # CFG1 shape (W = 4)
+    (96, 15000, 48, 10, 6, 10, 200),      # CFG3/CFG5 dim (W = 3)
+    (960, 6000, 16, 4, 4, 100, 1000),     # CFG2 dim (W = 30), M > list sizes
+    (33, 4000, 10, 8, 3, 5, 40),          # ragged W = 2 (generic path)
+])
+def test_stage_parity(orc, D, N, nlist, nq, nprobe, k, M):
+    X, Q = make_data(D, N, nlist, nq)
+    idx = build(X, nlist)
+    _stage_checks(orc, idx, X, Q, k, nprobe, M)
+
+
+def test_stage_parity_lower_bound_key(orc):
+    X, Q = make_data(128, 12000, 32, 8)
+    idx = build(X, 32)
+    _stage_checks(orc, idx, X, Q, 10, 6, 80, rank_key=1)
+
+
+def test_cfg1_end_to_end(orc):
+    """CFG1 at full size (N = 1e5, D = 128, nlist 256, 100 queries, nprobe 16,
+    k 10, M 100): GPU vs the oracle running the whole path independently (its
+    own fp64 rotation and probing) on the exported index; recall vs exact kNN."""
+    s = synth.spec(1)
+    cen = synth.centres(s, "cpu")
+    X = synth.base_rows(s, 0, s.N, "cpu", cen=cen)
+    Q = synth.queries(s, "cpu", cen=cen)
+    idx = build(X, s.nlist)
+    ex = idx.export()
+    ids, d = idx.search(Q.cuda(), s.k, s.nprobe, s.M)
+    ids, d = ids.cpu().numpy(), d.cpu().numpy()
+    oi, od = orc.search(Q.numpy(), ex["rotation"], ex["centroids"], ex["list_off"], ex["ids"], ex["codes"],
+                        ex["n_o"], ex["rho"], X.numpy(), s.k, s.nprobe, s.M, SEED)
+    same = np.mean([np.array_equal(a, b) for a, b in zip(ids, oi)])
+    assert same >= 0.95, same
+    gt, _ = orc.bruteforce(X.numpy(), Q.numpy(), s.k)
+    rg, ro = pu.recall(ids, gt, s.k), pu.recall(oi, gt, s.k)
+    assert abs(rg - ro) <= 0.01, (rg, ro)
+    assert rg >= 0.85, rg
+    # host-buffer (end-to-end) call path returns the same answer
+    hi, hd = idx.search(Q, s.k, s.nprobe, s.M)
+    assert np.array_equal(hi.numpy(), ids) and np.array_equal(hd.numpy(), d)
+
+
+def test_exhaustive_is_exact_knn(orc):
+    """nprobe = nlist and M >= N -> exact kNN."""
+    X, Q = make_data(64, 3000, 12, 10)
+    idx = build(X, 12)
+    ids, d = idx.search(Q.cuda(), 10, 12, 3000)
+    gi, gd = orc.bruteforce(X.numpy(), Q.numpy(), 10)
+    pu.check_final(ids.cpu().numpy(), d.cpu().numpy(), gi, gd.astype(np.float32), 10)
+
+
+def test_invariances(orc):
+    """Results do not depend on batch split (query_id_base), survivor buffer
+    size (forced overflow re-scans), threshold seeding size."""
+    X, Q = make_data(128, 20000, 64, 40)
+    idx = build(X, 64)
+    Qd = Q.cuda()
+    base_i, base_d = idx.search(Qd, 10, 8, 100)
+    a_i, a_d = idx.search(Qd[:17], 10, 8, 100)
+    b_i, b_d = idx.search(Qd[17:], 10, 8, 100, query_id_base=17)
+    assert torch.equal(torch.cat([a_i, b_i]), base_i) and torch.equal(torch.cat([a_d, b_d]), base_d)
+    retries = torch.zeros(1, dtype=torch.int32, device="cuda")
+    c_i, c_d = idx.search(Qd, 10, 8, 100, cap=101, debug=dict(retries=retries))
+    assert torch.equal(c_i, base_i) and torch.equal(c_d, base_d)
+    assert int(retries.item()) >= 1  # the overflow path ran
+    s_i, s_d = idx.search(Qd, 10, 8, 100, seed_max=100)
+    assert torch.equal(s_i, base_i) and torch.equal(s_d, base_d)
+
+
+def test_edge_cases():
+    X, Q = make_data(32, 500, 50, 6)
+    idx = build(X, 50)
+    # nq = 0
+    i0, d0 = idx.search(Q[:0].cuda(), 5, 3, 10)
+    assert i0.shape == (0, 5)
+    # fewer candidates than k -> (-1, +inf) padding
+    ids, d = idx.search(Q.cuda(), 64, 1, 64)
+    ids, d = ids.cpu().numpy(), d.cpu().numpy()
+    for q in range(6):
+        n = int((ids[q] >= 0).sum())
+        assert np.all(ids[q, n:] == -1) and np.all(np.isinf(d[q, n:])) and np.all(np.isfinite(d[q, :n]))
+    # errors
+    with pytest.raises(rq.RabitqError) as e:
+        idx.search(Q.cuda(), 0, 3, 10)
+    assert e.value.status == rq.ERR_INVALID_ARGUMENT
+    with pytest.raises(rq.RabitqError):
+        idx.search(Q.cuda(), 10, 3, 5)  # n_rerank < k
+    with pytest.raises(rq.RabitqError):
+        idx.search(Q.cuda(), 10, 51, 20)  # nprobe > nlist
+    bad = Q.clone()
+    bad[2, 3] = float("nan")
+    with pytest.raises(rq.RabitqError) as e:
+        idx.search(bad.cuda(), 5, 3, 10)
+    assert e.value.status == rq.ERR_INVALID_DATA
+    Xb = X.clone()
+    Xb[0, 0] = float("inf")
+    with pytest.raises(rq.RabitqError) as e:
+        rq.Index(Xb.cuda(), nlist=10)
+    assert e.value.status == rq.ERR_INVALID_DATA
+    with pytest.raises(rq.RabitqError):
+        rq.Index(X[:5].cuda(), nlist=10)  # n < nlist
+
+
+def test_merge_topk_kernel(orc):
+    rng = np.random.default_rng(3)
+    G, nq, k = 4, 9, 10
+    ids = rng.permutation(100000)[: G * nq * k].reshape(G, nq, k).astype(np.int64)
+    d = np.sort(rng.integers(0, 30, (G, nq, k)).astype(np.float32), -1)
+    oi, od = rq.merge_topk(torch.from_numpy(ids).cuda(), torch.from_numpy(d).cuda())
+    ri, rd = orc.merge_topk(ids, d)
+    assert np.array_equal(oi.cpu().numpy(), ri) and np.array_equal(od.cpu().numpy(), rd)
+
+
+def test_borrow_and_shard_offsets(orc):
+    """A shard built over a contiguous id slice (id_offset, shared P and
+    centroids) returns global ids; borrowed vectors re-rank identically."""
+    X, Q = make_data(64, 8000, 20, 6)
+    full = build(X, 20)
+    ex = full.export()
+    Xd = X.cuda()
+    lo, hi = 3000, 8000
+    shard = rq.Index(Xd[lo:hi], nlist=20, seed=SEED, id_offset=lo, rotation=ex["rotation"],
+                     centroids_rot=ex["centroids"], borrow=True)
+    ids, d = shard.search(Q.cuda(), 10, 20, 5000)
+    ids = ids.cpu().numpy()
+    assert ids.min() >= lo and ids.max() < hi
+    gi, gd = orc.bruteforce(X.numpy()[lo:hi], Q.numpy(), 10)
+    pu.check_final(ids, d.cpu().numpy(), gi + lo, gd.astype(np.float32), 10)

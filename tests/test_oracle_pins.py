@@ -571,3 +571,20 @@ def test_padding_when_fewer_candidates(orc):
         if n < 50:
             assert np.all(ids[q, n:] == -1) and np.all(np.isinf(d[q, n:]))
             assert np.all(ids[q, :n] >= 0)
+
+
+def test_rerank_is_restricted_bruteforce(orc):
+    """Fine ranking over a candidate set = brute force restricted to it (S:L337);
+    over all ids it is exact kNN (numpy, direct subtraction)."""
+    X, Q = _mixture(35, 1500, 20, 6, 12)
+    allc = np.tile(np.arange(1500, dtype=np.int64), (12, 1))
+    ids, d = orc.rerank(Q, X, allc, 7)
+    rid, rd = _np_knn(X, Q, 7)
+    assert np.array_equal(ids, rid) and np.allclose(d, rd.astype(np.float32), rtol=1e-6)
+    sub = np.stack([np.random.default_rng(q).choice(1500, 40, replace=False) for q in range(12)])
+    sub[:, -3:] = -1  # skipped entries
+    ids2, _ = orc.rerank(Q, X, sub, 5)
+    for q in range(12):
+        s = sub[q][sub[q] >= 0]
+        dd = ((X[s].astype(np.float64) - Q[q].astype(np.float64)) ** 2).sum(1)
+        assert np.array_equal(ids2[q], s[np.lexsort((s, dd))][:5])
