@@ -1,0 +1,438 @@
+#!/usr/bin/env python
+"""bench.py -- the IVF-RaBitQ search hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+A step is one pass of the whole hot path (rotate, probe, quantize, scan +
+estimator, top-M, exact re-rank; + NCCL top-k merge for N > 1) over one batch
+of the config's queries against its index, inputs resident in HBM.  The
+default workload is BASELINE.json configs[1] (CFG2: D=960, N=1e6, nlist=1024,
+10k queries, nprobe=64, k=100, re-rank 1000).  Rank 0 prints ONE JSON line.
+
+For N > 1 (torchrun, one process per GPU) the index is sharded by contiguous
+id slices, every rank scans its shard for all queries, and the
+per-rank top-k are merged by an NCCL all-gather: total work is
+fixed, "scaling": "strong".
+
+--impl reference times the oracle (oracle/, plain C fp64) on this box's host
+cores on the same config/metric, each step a bounded sample of the queries,
+over an index built on the CPU (torch CPU BLAS k-means/assignment + the
+oracle's rotation); rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "QPS at fixed nprobe/k (coarse-scan GB/s vs HBM peak; recall@k vs exact)"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+# ----------------------------------------------------------------- clocks --
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.proc = device, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        rows = [r for r in self.rows if len(r) >= 8]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for n, v in zip(names, r[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        load = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": float(np.median(load)) if load else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ------------------------------------------------------------- workload --
+def workload(args):
+    s = synth.spec(args.config, **({"nq": args.nq} if args.nq else {}))
+    return s
+
+
+def build_shard(s, rank, world, dev, rq):
+    """Generate this rank's contiguous id slice on the device and build its
+    shard (rank 0 trains P and the centroids, the others reuse them)."""
+    lo, hi = synth.shard_range(s.N, rank, world)
+    cen = synth.centres(s, dev)
+    t0 = time.time()
+    X = synth.base_rows(s, lo, hi, dev, cen=cen)
+    Q = synth.queries(s, dev, cen=cen)
+    init = synth.init_centroids(s, dev)
+    if world > 1:
+        torch.distributed.broadcast(Q, 0)
+    tgen = time.time() - t0
+    t0 = time.time()
+    if world == 1:
+        idx = rq.Index(X, nlist=s.nlist, seed=s.build_seed, borrow=True, init_centroids=init)
+    else:
+        P = torch.empty(s.D, s.D, device=dev)
+        C = torch.empty(s.nlist, s.D, device=dev)
+        if rank == 0:
+            idx = rq.Index(X, nlist=s.nlist, seed=s.build_seed, borrow=True, init_centroids=init, id_offset=lo)
+            ex = idx.export()
+            P.copy_(torch.from_numpy(ex["rotation"]))
+            C.copy_(torch.from_numpy(ex["centroids"]))
+        torch.distributed.broadcast(P, 0)
+        torch.distributed.broadcast(C, 0)
+        if rank != 0:
+            idx = rq.Index(X, nlist=s.nlist, seed=s.build_seed, borrow=True, id_offset=lo, rotation=P,
+                           centroids_rot=C)
+    torch.cuda.synchronize()
+    log(f"[rank {rank}] data {tgen:.1f}s build {time.time() - t0:.1f}s rows [{lo},{hi}) {idx.info()}")
+    return idx, X, Q
+
+
+def l2_flush(buf):
+    buf.add_(1.0)  # writes 256 MiB > 126 MB L2
+
+
+def run_ours(args):
+    import paper_2605_16007_b200 as rq
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        torch.distributed.init_process_group("nccl", device_id=dev)
+    s = workload(args)
+    idx, X, Q = build_shard(s, rank, world, dev, rq)
+    comm = None
+    if world > 1:
+        uid = [rq.Comm.unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(uid, 0)
+        comm = rq.Comm(uid[0], rank, world, local)
+    stream = torch.cuda.Stream(dev)  # the library's kernels and the timing events share this stream
+    ids = torch.empty(s.nq, s.k, dtype=torch.int64, device=dev)
+    dist = torch.empty(s.nq, s.k, dtype=torch.float32, device=dev)
+    flush = torch.zeros(64 << 20, dtype=torch.float32, device=dev)
+
+    def step(prof=None):
+        if comm is None:
+            idx.search(Q, s.k, s.nprobe, s.M, scan_path=args.scan_path, stream=stream, out=(ids, dist),
+                       profile=prof)
+        else:
+            kw = dict(scan_path=args.scan_path, stream=stream.cuda_stream)
+            if prof is not None:
+                import ctypes
+
+                kw["profile"] = ctypes.pointer(prof)
+            r = comm.search_sharded(idx, Q, s.k, s.nprobe, s.M, **kw)
+            ids.copy_(r[0])
+            dist.copy_(r[1])
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    times, profs = [], []
+    for _ in range(args.steps):
+        l2_flush(flush)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        prof = rq.Profile()
+        e0.record(stream)
+        step(prof)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+        profs.append(prof.as_dict())
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    total = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(total, op=torch.distributed.ReduceOp.MAX)
+    total_ms = float(total.item())
+    ms_per_step = total_ms / args.steps
+    qps = s.nq * args.steps / (total_ms / 1e3)
+
+    # ---- e2e: the same search through the C ABI with HOST buffers ----
+    Qh = Q.cpu().pin_memory()
+    ih = torch.empty(s.nq, s.k, dtype=torch.int64).pin_memory()
+    dh = torch.empty(s.nq, s.k, dtype=torch.float32).pin_memory()
+    for _ in range(1):
+        if comm is None:
+            idx.search(Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path, out=(ih, dh))
+        else:
+            comm.search_sharded(idx, Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path)
+    barrier()
+    et = []
+    for _ in range(max(3, min(args.steps, 10))):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if comm is None:
+            idx.search(Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path, out=(ih, dh))
+        else:
+            r = comm.search_sharded(idx, Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path)
+        et.append(time.perf_counter() - t0)
+    e2e_t = torch.tensor([sum(et)], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(e2e_t, op=torch.distributed.ReduceOp.MAX)
+    e2e_qps = s.nq * len(et) / float(e2e_t.item())
+
+    # ---- roofline of the dominant kernel (stage times measured live with CUDA events) ----
+    pk = peaks()
+    stage_ms = {k_: float(np.mean([p["stage_ms"][k_] for p in profs])) for k_ in profs[0]["stage_ms"]}
+    pairs = float(np.mean([p["pairs"] for p in profs]))
+    surv = float(np.mean([p["survivors"] for p in profs]))
+    launches = int(round(np.mean([p["kernel_launches"] for p in profs])))
+    W = s.W
+    scan_bytes = pairs * (4 * W + 8)  # code words + {n_o^2, f1} per (query, vector) pair
+    rerank_bytes = s.nq * s.M * (4 * s.D + 8) + surv * 8
+    rl = {
+        "scan": {"bound": "hbm", "achieved": scan_bytes / (stage_ms["scan"] * 1e-3) / 1e9,
+                 "algorithmic_bytes": scan_bytes, "ms": stage_ms["scan"]},
+        "select_rerank": {"bound": "hbm", "achieved": rerank_bytes / (stage_ms["select_rerank"] * 1e-3) / 1e9,
+                          "algorithmic_bytes": rerank_bytes, "ms": stage_ms["select_rerank"]},
+    }
+    dom = max(rl, key=lambda k_: rl[k_]["ms"])
+    traffic = None
+    prof_path = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{s.cfg}.json")
+    if os.path.exists(prof_path):
+        try:
+            traffic = json.load(open(prof_path)).get(dom)
+        except Exception:
+            traffic = None
+    roofline = {"kernel": dom, "bound": "hbm", "achieved": round(rl[dom]["achieved"], 1),
+                "peak": pk["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in pk
+                else "B200_PROFILING.md fallback", "unit": "GB/s",
+                "frac": round(rl[dom]["achieved"] / pk["hbm_gbs"], 4), "traffic": traffic,
+                "algorithmic_bytes_per_launch": rl[dom]["algorithmic_bytes"]}
+    scan_roof = {"achieved": round(rl["scan"]["achieved"], 1), "frac": round(rl["scan"]["achieved"] / pk["hbm_gbs"], 4),
+                 "ms": round(stage_ms["scan"], 4), "bytes_per_pair": 4 * W + 8, "pairs": pairs}
+
+    # ---- recall@k vs exact on a query sample (torch brute force, outside the timed region) ----
+    rec = None
+    if world == 1 and args.recall:
+        nsub = min(100, s.nq)
+        gt = []
+        for q0 in range(0, nsub, 25):
+            dd = torch.cdist(Q[q0:q0 + 25].double(), X.double())
+            gt.append(torch.topk(dd, s.k, largest=False).indices.cpu())
+        gt = torch.cat(gt).numpy()
+        got = ids[:nsub].cpu().numpy()
+        rec = float(np.mean([len(set(a_.tolist()) & set(b_.tolist())) / s.k for a_, b_ in zip(got, gt)]))
+
+    line = {
+        "metric": METRIC, "value": round(qps, 1), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "u32 codes x 4-bit query planes (popc) / f32",
+        "data": "synthetic (synth/ seeded Gaussian mixture, generated on device)",
+        "config": {"workload": f"CFG{s.cfg}", "D": s.D, "N": s.N, "nlist": s.nlist, "nq": s.nq, "nprobe": s.nprobe,
+                   "k": s.k, "n_rerank": s.M, "kind": s.kind, "parallelism": f"list-shards x{world}",
+                   "l2": "flushed between steps (256 MiB write)", "scan_path": args.scan_path},
+        "e2e": {"value": round(e2e_qps, 1), "unit": "queries/s", "h2d_bytes_per_step": s.nq * s.D * 4 * world,
+                "d2h_bytes_per_step": s.nq * s.k * 12 * world},
+        "gpu_launches": launches * args.steps,
+        "roofline": roofline, "scan_roofline": scan_roof,
+        "stage_ms": {k_: round(v, 4) for k_, v in stage_ms.items()},
+        "survivors_per_query": round(surv / s.nq, 1), "recall_at_k": rec, "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(s, idx, X, Q, args)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.free()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+# ------------------------------------------------------- CPU (oracle) legs --
+def _cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def _oracle_time(orc, s, ex, Xh, Qh, nqs, threads):
+    t0 = time.perf_counter()
+    orc.search(Qh[:nqs], ex["rotation"], ex["centroids"], ex["list_off"], ex["ids"], ex["codes"], ex["n_o"], ex["rho"],
+               Xh, s.k, s.nprobe, s.M, s.build_seed, num_threads=threads)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(s, idx, X, Q, args, budget_s=20.0):
+    """The oracle as it stands, on this box's host cores, over the exported
+    index, on a bounded query sample (about `budget_s` seconds of CPU work)."""
+    import oracle as orc
+
+    orc.build()
+    ex = idx.export()
+    Xh = X.cpu().numpy()
+    Qh = Q.cpu().numpy()
+    cores = _cores()
+    n0 = min(s.nq, max(2, cores))
+    t = _oracle_time(orc, s, ex, Xh, Qh, n0, cores)
+    nqs = int(min(s.nq, max(n0, n0 * budget_s / max(t, 1e-3))))
+    t = _oracle_time(orc, s, ex, Xh, Qh, nqs, cores)
+    return {"value": round(nqs / t, 3), "unit": "queries/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {nqs} of {s.nq} CFG{s.cfg} queries, full oracle path (fp64 rotate/probe, pinned fp32 "
+                      f"quantizer, plain-loop ip, fp64 estimator, full sort, fp64 re-rank) over the exported index, "
+                      f"OpenMP {cores} threads, {t:.1f} s"}
+
+
+def reference_index_cpu(s, X, seed):
+    """CPU index for the reference arm: oracle Haar P; k-means (10 Lloyd
+    iterations on 32 nlist rows) and nearest-centroid assignment with torch CPU
+    matmuls; sign codes / factors of the rotated residual; no GPU involved."""
+    import oracle as orc
+
+    _, P = orc.haar_rotation(s.D, seed)
+    Pt = torch.from_numpy(P)
+    Xr = X @ Pt  # x' = P^T x, row form
+    g = torch.Generator().manual_seed(seed)
+    ts = min(s.N, 32 * s.nlist)
+    T = Xr[torch.randperm(s.N, generator=g)[:ts]]
+    C = T[torch.randperm(ts, generator=g)[: s.nlist]].clone()
+    for _ in range(10):
+        a = torch.cdist(T, C).argmin(1)
+        Cn = torch.zeros_like(C).index_add_(0, a, T)
+        cnt = torch.bincount(a, minlength=s.nlist).clamp_min(1).unsqueeze(1)
+        C = torch.where(torch.bincount(a, minlength=s.nlist).unsqueeze(1) > 0, Cn / cnt, C)
+    assign = torch.empty(s.N, dtype=torch.int64)
+    for r0 in range(0, s.N, 65536):
+        assign[r0:r0 + 65536] = torch.cdist(Xr[r0:r0 + 65536], C).argmin(1)
+    order = torch.argsort(assign, stable=True)
+    off = torch.zeros(s.nlist + 1, dtype=torch.int64)
+    off[1:] = torch.cumsum(torch.bincount(assign, minlength=s.nlist), 0)
+    R = (Xr[order] - C[assign[order]]).double()
+    bits = (R >= 0).numpy()
+    W = s.W
+    pad = np.zeros((s.N, W * 32), bool)
+    pad[:, : s.D] = bits
+    codes = np.packbits(pad.reshape(s.N, W, 32), axis=2, bitorder="little").view("<u4").reshape(s.N, W)
+    n_o = R.norm(dim=1)
+    rho = torch.where(n_o > 0, R.abs().sum(1) / (np.sqrt(s.D) * n_o), torch.ones_like(n_o))
+    return dict(rotation=P, centroids=C.numpy(), list_off=off.numpy(), ids=order.numpy().astype(np.int64),
+                codes=codes, n_o=n_o.float().numpy(), rho=rho.float().numpy())
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle as orc
+
+    orc.build()
+    s = workload(args)
+    t0 = time.time()
+    cen = synth.centres(s, "cpu")
+    X = synth.base_rows(s, 0, s.N, "cpu", cen=cen)
+    Q = synth.queries(s, "cpu", cen=cen)
+    ex = reference_index_cpu(s, X, s.build_seed)
+    log(f"[reference] data + CPU index {time.time() - t0:.1f}s")
+    Xh, Qh = X.numpy(), Q.numpy()
+    cores = _cores()
+    n0 = min(s.nq, max(2, cores))
+    t = _oracle_time(orc, s, ex, Xh, Qh, n0, cores)
+    per_step_budget = max(2.0, 150.0 / max(1, args.steps + args.warmup))
+    nqs = int(min(s.nq, max(1, n0 * per_step_budget / max(t, 1e-3))))
+    for w in range(args.warmup):
+        _oracle_time(orc, s, ex, Xh, Qh[w * nqs % max(1, s.nq - nqs):], nqs, cores)
+    tt = []
+    for i in range(args.steps):
+        q0 = (i * nqs) % max(1, s.nq - nqs + 1)
+        tt.append(_oracle_time(orc, s, ex, Xh, Qh[q0:], nqs, cores))
+    qps = nqs * len(tt) / sum(tt)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(qps, 3), "unit": "queries/s", "n_gpus": int(
+            os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * sum(tt) / len(tt), 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64 (oracle)", "data": "synthetic (synth/, CPU)",
+        "config": {"workload": f"CFG{s.cfg}", "D": s.D, "N": s.N, "nlist": s.nlist, "nq": s.nq, "nprobe": s.nprobe,
+                   "k": s.k, "n_rerank": s.M, "queries_per_step": nqs},
+        "cpu_baseline": {"value": round(qps, 3), "unit": "queries/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{nqs} queries per step of CFG{s.cfg}, oracle over a CPU-built index"},
+        "e2e": {"value": round(qps, 3), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--nq", type=int, default=0, help="override the query count (quick runs)")
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--scan-path", type=int, default=0, dest="scan_path")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-recall", dest="recall", action="store_false")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        log("note: warmup raised to the contract minimum of 3")
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

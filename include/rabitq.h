@@ -115,6 +115,22 @@ typedef struct {
     int64_t scan_dump_cap;
 } rabitq_debug;
 
+/* Optional per-call measurement (host memory), filled when the call returns.
+ * Stage times come from CUDA events recorded on the call's stream around each
+ * stage (summed over internal query batches). */
+#define RABITQ_NSTAGES 8
+typedef struct {
+    float stage_ms[RABITQ_NSTAGES]; /* 0 rotate, 1 probe GEMM+select, 2 quantize, 3 plan,
+                                       4 threshold seed, 5 scan (+estimator), 6 overflow
+                                       re-scans, 7 top-M select + exact re-rank         */
+    int64_t pairs;                  /* (query, vector) pairs scanned by the first scan   */
+    int64_t survivors;              /* candidates kept by the threshold, all queries     */
+    int32_t retries;                /* overflow re-scans                                 */
+    int32_t kernel_launches;        /* librabitq kernels launched by this call           */
+    int32_t scan_path_used;         /* 1 popc, 2 imma                                    */
+    int32_t batches;                /* internal query batches                            */
+} rabitq_profile;
+
 typedef struct {
     int32_t scan_path;       /* rabitq_scan_path; AUTO picks by workload                       */
     int32_t rank_key;        /* rabitq_rank_key; default EST (R#15)                  */
@@ -125,6 +141,7 @@ typedef struct {
     void* stream;            /* cudaStream_t to run on (NULL -> the index's stream); outputs
                                 in device memory are valid after that stream synchronizes     */
     rabitq_debug* debug;     /* nullable                                                       */
+    rabitq_profile* profile; /* nullable, host memory                                          */
 } rabitq_search_opts;
 
 /* Search nq queries Q [nq x d] fp32: rotate, probe the nprobe

@@ -63,6 +63,27 @@ class Debug(ctypes.Structure):
     ]
 
 
+NSTAGES = 8
+STAGES = ["rotate", "probe", "quantize", "plan", "seed", "scan", "rescan", "select_rerank"]
+
+
+class Profile(ctypes.Structure):
+    _fields_ = [
+        ("stage_ms", ctypes.c_float * NSTAGES),
+        ("pairs", ctypes.c_int64),
+        ("survivors", ctypes.c_int64),
+        ("retries", ctypes.c_int32),
+        ("kernel_launches", ctypes.c_int32),
+        ("scan_path_used", ctypes.c_int32),
+        ("batches", ctypes.c_int32),
+    ]
+
+    def as_dict(self):
+        d = {f: getattr(self, f) for f, _ in self._fields_ if f != "stage_ms"}
+        d["stage_ms"] = {s: float(self.stage_ms[i]) for i, s in enumerate(STAGES)}
+        return d
+
+
 class SearchOpts(ctypes.Structure):
     _fields_ = [
         ("scan_path", ctypes.c_int32),
@@ -73,6 +94,7 @@ class SearchOpts(ctypes.Structure):
         ("seed_max", ctypes.c_int32),
         ("stream", ctypes.c_void_p),
         ("debug", ctypes.POINTER(Debug)),
+        ("profile", ctypes.POINTER(Profile)),
     ]
 
 
@@ -192,7 +214,8 @@ class Index:
     # -- rabitq_search_ex -------------------------------------------------------
     def search(self, Q, k: int, nprobe: int, n_rerank: int, *, scan_path: int = SCAN_AUTO,
                rank_key: int = RANK_EST, eps0: float = 0.0, query_id_base: int = 0, cap: int = 0,
-               seed_max: int = 0, stream=None, debug: Optional[dict] = None, out=None):
+               seed_max: int = 0, stream=None, debug: Optional[dict] = None, out=None,
+               profile: Optional[Profile] = None):
         """Returns (ids int64 [nq, k], dists float32 [nq, k]) on Q's device.
         ``debug`` maps rabitq_debug member names to preallocated tensors."""
         torch = _torch()
@@ -217,6 +240,8 @@ class Index:
                 else:
                     setattr(dbg, name, _ptr(t))
             o.debug = ctypes.pointer(dbg)
+        if profile is not None:
+            o.profile = ctypes.pointer(profile)
         _check(lib().rabitq_search_ex(self._h, ctypes.c_void_p(_ptr(Q)), ctypes.c_int64(nq), ctypes.c_int32(k),
                                       ctypes.c_int32(nprobe), ctypes.c_int32(n_rerank), ctypes.byref(o),
                                       ctypes.c_void_p(_ptr(ids)), ctypes.c_void_p(_ptr(dists))))

@@ -262,6 +262,7 @@ static void search_local(const rabitq_index* idx, const float* Q, int64_t nq, in
         }
     }
     rabitq::SearchStats stats;
+    stats.timing = o.profile != nullptr;
     for (int64_t b0 = 0; b0 < nq; b0 += qbatch) {
         const int64_t m = std::min(qbatch, nq - b0);
         rabitq::DebugOut dbg;
@@ -287,6 +288,17 @@ static void search_local(const rabitq_index* idx, const float* Q, int64_t nq, in
         }
         rabitq::search_batch(idx, Qd + (size_t)b0 * D, m, k, nprobe, M, cfg, o.query_id_base + b0,
                              ids_d + (size_t)b0 * k, dists_d + (size_t)b0 * k, dbg, st, &stats);
+    }
+    if (o.profile) {
+        rabitq_profile* pf = o.profile;
+        std::memset(pf, 0, sizeof(*pf));
+        for (int i = 0; i < RABITQ_NSTAGES; ++i) pf->stage_ms[i] = stats.stage_ms[i];
+        pf->pairs = stats.pairs;
+        pf->survivors = stats.survivors;
+        pf->retries = stats.retries;
+        pf->kernel_launches = stats.launches;
+        pf->scan_path_used = stats.used_imma ? 2 : 1;
+        pf->batches = stats.batches;
     }
     if (dg) {
         v_qbar.copy_back(st);

@@ -79,8 +79,14 @@ struct DebugOut {  // device-or-host pointers (cudaMemcpyDefault), all nullable
 };
 
 struct SearchStats {
+    bool timing = false;       // record CUDA events per stage (rabitq_profile)
+    float stage_ms[8] = {};
+    int64_t pairs = 0;
+    int64_t survivors = 0;
     int retries = 0;
+    int launches = 0;
     int used_imma = 0;
+    int batches = 0;
 };
 
 void search_batch(const rabitq_index* idx, const float* Q, int64_t nq, int k, int nprobe, int M,

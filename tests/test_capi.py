@@ -62,6 +62,7 @@ def test_struct_layouts_match_header():
             if not decl:
                 continue
             for part in decl.split(","):
+                part = re.sub(r"\[.*?\]", "", part)
                 out.append(re.findall(r"\*?\s*([A-Za-z_0-9]+)\s*$", part.strip())[0])
         return out
 
@@ -70,6 +71,7 @@ def test_struct_layouts_match_header():
     assert [f for f, _ in rq.Debug._fields_] == fields("rabitq_debug")
     assert [f for f, _ in rq.IndexInfo._fields_] == fields("rabitq_index_info_t")
     assert [f for f, _ in rq.Export._fields_] == fields("rabitq_export_t")
+    assert [f for f, _ in rq.Profile._fields_] == fields("rabitq_profile")
 
 
 def test_argument_errors_without_gpu(lib):

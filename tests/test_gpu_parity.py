@@ -13,7 +13,7 @@ import pytest
 import torch
 
 import synth
-from tests import parity_util as pu
+import parity_util as pu
 
 pytestmark = pytest.mark.gpu
 
@@ -95,8 +95,13 @@ def test_build_parity(orc, D, N, nlist):
         mine = d[np.arange(N), assign]
         assert np.all(mine <= best + 1e-4 * np.maximum(best, 1.0))
     codes, n_o, rho = orc.encode(Xn[ids], P, Cr, assign[ids])
-    # codes identical except bits whose rotated residual is ~0 (fp32 GEMM vs fp64)
+    # The GPU forms r_o = x' - c' from an fp32 GEMM x' (P:L324 restructuring);
+    # its rounding is ~ sqrt(D) eps32 ||x||, so a bit may differ only where the
+    # fp64 residual is within that scale of 0.
+    xs = np.linalg.norm(Xn[ids].astype(np.float64), axis=1)
+    scale = 8 * math.sqrt(D) * 2.0 ** -24 * (xs + np.linalg.norm(Cr[assign[ids]].astype(np.float64), axis=1))
     diff = codes ^ ex["codes"]
+    nflip = 0
     if diff.any():
         r = Xr[ids] - Cr[assign[ids]].astype(np.float64)
         rows, words = np.nonzero(diff)
@@ -105,9 +110,12 @@ def test_build_parity(orc, D, N, nlist):
             for b in range(32):
                 if bits >> b & 1:
                     i = 32 * w + b
-                    assert abs(r[v, i]) <= 1e-5 * n_o[v] + 1e-6, (v, i, r[v, i])
-    assert np.allclose(ex["n_o"], n_o, rtol=1e-5, atol=1e-6)
-    assert np.allclose(ex["rho"], rho, rtol=1e-5, atol=1e-6)
+                    assert abs(r[v, i]) <= scale[v], (v, i, r[v, i], scale[v])
+                    nflip += 1
+    assert nflip <= 1e-4 * N * D
+    assert np.all(np.abs(ex["n_o"] - n_o) <= 1e-5 * n_o + math.sqrt(D) * scale)
+    ok = n_o > 1e3 * scale  # rho of a residual at rounding-noise scale is itself noise (R#27)
+    assert np.allclose(ex["rho"][ok], rho[ok], rtol=1e-5, atol=1e-6)
 
 
 def _stage_checks(orc, idx, X, Q, k, nprobe, M, rank_key=0):
@@ -243,7 +251,7 @@ def test_invariances(orc):
     b_i, b_d = idx.search(Qd[17:], 10, 8, 100, query_id_base=17)
     assert torch.equal(torch.cat([a_i, b_i]), base_i) and torch.equal(torch.cat([a_d, b_d]), base_d)
     retries = torch.zeros(1, dtype=torch.int32, device="cuda")
-    c_i, c_d = idx.search(Qd, 10, 8, 100, cap=101, debug=dict(retries=retries))
+    c_i, c_d = idx.search(Qd, 10, 8, 100, cap=101, seed_max=100, debug=dict(retries=retries))
     assert torch.equal(c_i, base_i) and torch.equal(c_d, base_d)
     assert int(retries.item()) >= 1  # the overflow path ran
     s_i, s_d = idx.search(Qd, 10, 8, 100, seed_max=100)
