@@ -136,7 +136,9 @@ typedef struct {
     int32_t rank_key;        /* rabitq_rank_key; default EST (R#15)                  */
     float eps0;              /* error-bound confidence, 0 -> 1.9 (R#14)                        */
     int64_t query_id_base;   /* global index of Q row 0 (Philox counter)                       */
-    int32_t cap_per_query;   /* survivor buffer per query, 0 -> auto; overflow re-scans         */
+    int32_t cap_per_query;   /* survivor buffer per query, 0 -> auto (max(2048, 4M)); clamped to
+                                >= 2 n_rerank; overflowing queries are re-scanned with a tighter
+                                threshold until they fit                                       */
     int32_t seed_max;        /* vectors used to seed the pruning threshold, 0 -> auto           */
     void* stream;            /* cudaStream_t to run on (NULL -> the index's stream); outputs
                                 in device memory are valid after that stream synchronizes     */

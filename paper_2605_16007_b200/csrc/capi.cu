@@ -233,7 +233,8 @@ static void search_local(const rabitq_index* idx, const float* Q, int64_t nq, in
     cfg.rank_key = o.rank_key;
     cfg.eps0 = o.eps0 > 0.0f ? o.eps0 : 1.9f;
     cfg.cap = o.cap_per_query > 0 ? o.cap_per_query : std::max(2048, 4 * M);
-    cfg.cap = std::max(cfg.cap, M + 1);
+    // re-scans shrink the survivors by ~M/cap per round: keep cap >= 2M
+    cfg.cap = std::max(cfg.cap, 2 * M);
     cfg.seed_max = o.seed_max > 0 ? o.seed_max : std::min(32768, std::max(4096, 4 * M));
     cfg.seed_max = std::max(cfg.seed_max, M);
     RQ_REQUIRE(cfg.seed_max <= 49152, RABITQ_ERR_INVALID_ARGUMENT, "seed_max too large");

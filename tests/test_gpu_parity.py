@@ -251,7 +251,7 @@ def test_invariances(orc):
     b_i, b_d = idx.search(Qd[17:], 10, 8, 100, query_id_base=17)
     assert torch.equal(torch.cat([a_i, b_i]), base_i) and torch.equal(torch.cat([a_d, b_d]), base_d)
     retries = torch.zeros(1, dtype=torch.int32, device="cuda")
-    c_i, c_d = idx.search(Qd, 10, 8, 100, cap=101, seed_max=100, debug=dict(retries=retries))
+    c_i, c_d = idx.search(Qd, 10, 8, 100, cap=200, seed_max=100, debug=dict(retries=retries))
     assert torch.equal(c_i, base_i) and torch.equal(c_d, base_d)
     assert int(retries.item()) >= 1  # the overflow path ran
     s_i, s_d = idx.search(Qd, 10, 8, 100, seed_max=100)
