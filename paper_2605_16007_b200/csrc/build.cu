@@ -147,14 +147,20 @@ __global__ void scatter_kernel(int64_t n, int D, int W, const int32_t* __restric
                                const float* __restrict__ no_id, const float* __restrict__ rho_id,
                                uint32_t* __restrict__ codes, float2* __restrict__ fac, float* __restrict__ g1,
                                float* __restrict__ n_o, float* __restrict__ rho, uint32_t* __restrict__ rows,
-                               uint32_t* __restrict__ slot_of_row) {
+                               uint32_t* __restrict__ slot_of_row, uint16_t* __restrict__ pcnt) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
         const int j = skeys[p];
         const uint32_t row = srows[p];
         const int64_t slot = slot_off[j] + (p - list_off[j]);
         const int64_t blk = slot >> 5;
         const int lane = (int)(slot & 31);
-        for (int w = 0; w < W; ++w) codes[((size_t)blk * W + w) * 32 + lane] = codes_id[(size_t)row * W + w];
+        int pc = 0;
+        for (int w = 0; w < W; ++w) {
+            const uint32_t cw = codes_id[(size_t)row * W + w];
+            codes[((size_t)blk * W + w) * 32 + lane] = cw;
+            pc += __popc(cw);
+        }
+        pcnt[slot] = (uint16_t)pc;
         const float no = no_id[row], rh = rho_id[row];
         const double dno = no, drh = rh;
         fac[slot] = make_float2((float)(dno * dno), (float)(2.0 * dno / (drh * sqrt((double)D))));
@@ -227,6 +233,8 @@ void free_index_memory(rabitq_index* idx) {
     cudaFree(idx->slot_off);
     cudaFree(idx->codes);
     cudaFree(idx->fac);
+    cudaFree(idx->pcnt);
+    idx->pcnt = nullptr;
     cudaFree(idx->g1);
     cudaFree(idx->n_o);
     cudaFree(idx->rho);
@@ -435,6 +443,8 @@ void build_index(rabitq_index* idx, const float* X, int64_t n, int D, int nlist,
                             cudaMemcpyHostToDevice, st));
     RQ_CUDA(cudaMalloc(&idx->codes, (size_t)alloc_slots * W * sizeof(uint32_t)));
     RQ_CUDA(cudaMalloc(&idx->fac, (size_t)alloc_slots * sizeof(float2)));
+    RQ_CUDA(cudaMalloc(&idx->pcnt, (size_t)alloc_slots * sizeof(uint16_t)));
+    RQ_CUDA(cudaMemsetAsync(idx->pcnt, 0, (size_t)alloc_slots * sizeof(uint16_t), st));
     RQ_CUDA(cudaMalloc(&idx->g1, (size_t)alloc_slots * sizeof(float)));
     RQ_CUDA(cudaMalloc(&idx->n_o, (size_t)alloc_slots * sizeof(float)));
     RQ_CUDA(cudaMalloc(&idx->rho, (size_t)alloc_slots * sizeof(float)));
@@ -463,7 +473,7 @@ void build_index(rabitq_index* idx, const float* X, int64_t n, int D, int nlist,
                                                 end_bit, st));
         scatter_kernel<<<grid_for(n), 256, 0, st>>>(n, D, W, skeys.p, svals.p, idx->list_off, idx->slot_off,
                                                     codes_id.p, no_id.p, rho_id.p, idx->codes, idx->fac, idx->g1,
-                                                    idx->n_o, idx->rho, idx->rows, idx->slot_of_row);
+                                                    idx->n_o, idx->rho, idx->rows, idx->slot_of_row, idx->pcnt);
         RQ_CHECK_LAUNCH();
         RQ_CUDA(cudaStreamSynchronize(st));
     }

@@ -18,7 +18,6 @@ struct ScanArgs {
     const uint32_t* rows;
     const uint4* planes;       // [npairs][W] {plane0..3} per 32-dim word
     const float4* qscal;       // [npairs] {v_l, Delta, ||r_q||^2, S_q}
-    const int8_t* qbar8;       // [npairs][Dpad] int8 quantized query (IMMA path)
     const float* tau;          // [nq] float threshold
     const uint64_t* tau64;     // [nq] 64-bit (key, row) threshold (retry)
     const int* flags;          // [nq] retry flags
@@ -30,7 +29,39 @@ struct ScanArgs {
     int32_t* dump_ip;          // debug: [items x 32] ip per (item, lane)
     float* dump_est;
     int64_t dump_cap;
+    // grouped tcgen05 path (scan_imma.cu)
+    int nlist;
+    int Dp;                    // D rounded up to 32 (K of the int8 MMA)
+    const int64_t* gstart;     // [nlist + 1] first grouped row of each list's pairs
+    const int32_t* gpair;      // [npairs] pair index of each grouped row
+    const uint8_t* qbar8;      // [(npairs + 128) x Dp] quantized queries, grouped by list
+    const int64_t* list_items; // [nlist + 1] prefix of (128-vector tile, 128-query group) items
+    const uint16_t* pcnt;      // [nslots] popcount of each code
 };
+
+template <typename T>
+struct WBuf {  // stream-ordered workspace buffer
+    T* p = nullptr;
+    cudaStream_t st = nullptr;
+    void alloc(size_t count, cudaStream_t s) {
+        st = s;
+        if (count) RQ_CUDA(cudaMallocAsync(&p, count * sizeof(T), s));
+    }
+    ~WBuf() {
+        if (p) cudaFreeAsync(p, st);
+    }
+};
+
+// list grouping of the (query, probe) pairs for the grouped scan
+struct Groups {
+    WBuf<int64_t> gcount, gstart, list_items, itemc;
+    WBuf<int32_t> gfill, gpos, gpair;
+    WBuf<uint8_t> qbar8;
+    int Dp = 0;
+};
+void prepare_groups(const rabitq_index* idx, const int32_t* probes, int64_t npairs, Groups& g, cudaStream_t st,
+                    int& launches);
+bool imma_wanted(const rabitq_index* idx, int64_t npairs, int scan_path);
 
 struct RerankArgs {
     const int* cnt;
@@ -92,8 +123,7 @@ struct SearchStats {
 void search_batch(const rabitq_index* idx, const float* Q, int64_t nq, int k, int nprobe, int M,
                   const SearchCfg& cfg, int64_t qid_base, int64_t* ids, float* dists, const DebugOut& dbg,
                   cudaStream_t st, SearchStats* stats);
-void scan_dispatch(const ScanArgs& a, const rabitq_index* idx, const SearchCfg& cfg, bool lb, bool dump,
-                   cudaStream_t st, SearchStats* stats);
+void scan_imma(const ScanArgs& a, bool lb, bool dump, cudaStream_t st);
 void scan_popc_entry(const ScanArgs& a, bool lb, bool retry, bool dump, cudaStream_t st);
 void merge_topk(const int64_t* in_ids, const float* in_d, int G, int64_t nq, int k, int64_t* out_ids,
                 float* out_d, cudaStream_t st);

@@ -118,13 +118,13 @@ def test_build_parity(orc, D, N, nlist):
     assert np.allclose(ex["rho"][ok], rho[ok], rtol=1e-5, atol=1e-6)
 
 
-def _stage_checks(orc, idx, X, Q, k, nprobe, M, rank_key=0):
+def _stage_checks(orc, idx, X, Q, k, nprobe, M, rank_key=0, scan_path=0):
     ex = idx.export()
     P, Cr, off, lids, codes = ex["rotation"], ex["centroids"], ex["list_off"], ex["ids"], ex["codes"]
     n_o, rho = ex["n_o"], ex["rho"]
     Qn, Xn = Q.numpy(), X.numpy()
     nq, D = Qn.shape
-    ids, d, dbg = debug_search(idx, Q, k, nprobe, M, rank_key=rank_key)
+    ids, d, dbg = debug_search(idx, Q, k, nprobe, M, rank_key=rank_key, scan_path=scan_path)
     qr, probes, qbar, qscal = dbg["qrot"], dbg["probes"], dbg["qbar"], dbg["qscal"]
     # S1 rotation: q' = P^T q within fp32 GEMM rounding
     ref_qr = orc.rotate(Qn, P)
@@ -188,22 +188,36 @@ def _stage_checks(orc, idx, X, Q, k, nprobe, M, rank_key=0):
     return ids, d, oi, od, dbg
 
 
+@pytest.mark.parametrize("scan_path", [rq.SCAN_POPC, rq.SCAN_IMMA])
 @pytest.mark.parametrize("D,N,nlist,nq,nprobe,k,M", [
     (128, 20000, 64, 12, 8, 10, 100),     # CFG1 shape (W = 4)
     (96, 15000, 48, 10, 6, 10, 200),      # CFG3/CFG5 dim (W = 3)
     (960, 6000, 16, 4, 4, 100, 1000),     # CFG2 dim (W = 30), M > list sizes
     (33, 4000, 10, 8, 3, 5, 40),          # ragged W = 2 (generic path)
+    (128, 30000, 8, 300, 5, 10, 100),     # many queries per list: multi-group, multi-tile
 ])
-def test_stage_parity(orc, D, N, nlist, nq, nprobe, k, M):
+def test_stage_parity(orc, D, N, nlist, nq, nprobe, k, M, scan_path):
     X, Q = make_data(D, N, nlist, nq)
     idx = build(X, nlist)
-    _stage_checks(orc, idx, X, Q, k, nprobe, M)
+    _stage_checks(orc, idx, X, Q, k, nprobe, M, scan_path=scan_path)
 
 
-def test_stage_parity_lower_bound_key(orc):
+@pytest.mark.parametrize("scan_path", [rq.SCAN_POPC, rq.SCAN_IMMA])
+def test_stage_parity_lower_bound_key(orc, scan_path):
     X, Q = make_data(128, 12000, 32, 8)
     idx = build(X, 32)
-    _stage_checks(orc, idx, X, Q, 10, 6, 80, rank_key=1)
+    _stage_checks(orc, idx, X, Q, 10, 6, 80, rank_key=1, scan_path=scan_path)
+
+
+@pytest.mark.parametrize("D", [96, 128, 960])
+def test_scan_paths_identical(D):
+    """The bit-plane popc scan and the tcgen05 int8 scan give bit-identical
+    results (exact integer ip, one estimator function): S:L352 invariance."""
+    X, Q = make_data(D, 40000 if D < 900 else 8000, 32, 256)
+    idx = build(X, 32)
+    a_i, a_d = idx.search(Q.cuda(), 10, 8, 200, scan_path=rq.SCAN_POPC)
+    b_i, b_d = idx.search(Q.cuda(), 10, 8, 200, scan_path=rq.SCAN_IMMA)
+    assert torch.equal(a_i, b_i) and torch.equal(a_d, b_d)
 
 
 def test_cfg1_end_to_end(orc):
