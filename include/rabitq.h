@@ -125,6 +125,7 @@ typedef struct {
                                        re-scans, 7 top-M select + exact re-rank         */
     int64_t pairs;                  /* (query, vector) pairs scanned by the first scan   */
     int64_t survivors;              /* candidates kept by the threshold, all queries     */
+    int64_t max_survivors;          /* largest per-query survivor count                  */
     int32_t retries;                /* overflow re-scans                                 */
     int32_t kernel_launches;        /* librabitq kernels launched by this call           */
     int32_t scan_path_used;         /* 1 popc, 2 imma                                    */
@@ -136,7 +137,7 @@ typedef struct {
     int32_t rank_key;        /* rabitq_rank_key; default EST (R#15)                  */
     float eps0;              /* error-bound confidence, 0 -> 1.9 (R#14)                        */
     int64_t query_id_base;   /* global index of Q row 0 (Philox counter)                       */
-    int32_t cap_per_query;   /* survivor buffer per query, 0 -> auto (max(2048, 4M)); clamped to
+    int32_t cap_per_query;   /* survivor buffer per query, 0 -> auto (max(8192, 16M)); clamped to
                                 >= 2 n_rerank; overflowing queries are re-scanned with a tighter
                                 threshold until they fit                                       */
     int32_t seed_max;        /* vectors used to seed the pruning threshold, 0 -> auto           */

@@ -72,6 +72,7 @@ class Profile(ctypes.Structure):
         ("stage_ms", ctypes.c_float * NSTAGES),
         ("pairs", ctypes.c_int64),
         ("survivors", ctypes.c_int64),
+        ("max_survivors", ctypes.c_int64),
         ("retries", ctypes.c_int32),
         ("kernel_launches", ctypes.c_int32),
         ("scan_path_used", ctypes.c_int32),

@@ -232,7 +232,9 @@ static void search_local(const rabitq_index* idx, const float* Q, int64_t nq, in
     cfg.scan_path = o.scan_path;
     cfg.rank_key = o.rank_key;
     cfg.eps0 = o.eps0 > 0.0f ? o.eps0 : 1.9f;
-    cfg.cap = o.cap_per_query > 0 ? o.cap_per_query : std::max(2048, 4 * M);
+    // the survivor buffer is cheap HBM (8 B/entry): size it so that overflow
+    // re-scans are rare even when the seeded threshold is loose
+    cfg.cap = o.cap_per_query > 0 ? o.cap_per_query : std::max(8192, 16 * M);
     // re-scans shrink the survivors by ~M/cap per round: keep cap >= 2M
     cfg.cap = std::max(cfg.cap, 2 * M);
     cfg.seed_max = o.seed_max > 0 ? o.seed_max : std::min(32768, std::max(4096, 4 * M));
@@ -296,6 +298,7 @@ static void search_local(const rabitq_index* idx, const float* Q, int64_t nq, in
         for (int i = 0; i < RABITQ_NSTAGES; ++i) pf->stage_ms[i] = stats.stage_ms[i];
         pf->pairs = stats.pairs;
         pf->survivors = stats.survivors;
+        pf->max_survivors = stats.max_survivors;
         pf->retries = stats.retries;
         pf->kernel_launches = stats.launches;
         pf->scan_path_used = stats.used_imma ? 2 : 1;

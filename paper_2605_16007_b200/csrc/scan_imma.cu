@@ -79,7 +79,6 @@ __global__ __launch_bounds__(kNT, kCTAsPerSM) void scan_imma_kernel(ScanArgs a) 
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = tmem_base_s;
-    const uint32_t idesc = tc::idesc_i8(kTM, kTN);
     uint32_t phase[2] = {0u, 0u};
     bool pending[2] = {false, false};
 
@@ -103,6 +102,8 @@ __global__ __launch_bounds__(kNT, kCTAsPerSM) void scan_imma_kernel(ScanArgs a) 
         const int64_t grow0 = a.gstart[j] + g * kTN;
         const int64_t rem = G - g * kTN;
         const int ncols = (int)(rem < kTN ? rem : kTN);
+        const int ncols16 = (ncols + 15) & ~15;  // UMMA N (M = 128 needs N % 16 == 0): no MMA work on empty columns
+        const uint32_t idesc = tc::idesc_i8(kTM, ncols16);
 
         // ---- per-column constants (one query per column) ----
         if (tid < kTN) {
@@ -152,9 +153,9 @@ __global__ __launch_bounds__(kNT, kCTAsPerSM) void scan_imma_kernel(ScanArgs a) 
                     *reinterpret_cast<uint4*>(dst + 128) = expand16(x >> 16);
                 }
             }
-            // B: 128 query rows x kbytes, 16-byte units by cp.async
+            // B: the group's query rows (ncols rounded up to 16) x kbytes, 16-byte units by cp.async
             {
-                const int units = kTN * (kbytes / 16);
+                const int units = ncols16 * (kbytes / 16);
                 const int per_row = kbytes / 16;
                 for (int u = tid; u < units; u += kNT) {
                     const int rr = u / per_row, k16 = u % per_row;
@@ -200,6 +201,7 @@ __global__ __launch_bounds__(kNT, kCTAsPerSM) void scan_imma_kernel(ScanArgs a) 
 #pragma unroll 1
             for (int h = 0; h < 2; ++h) {
                 const int col0 = colbase + h * 32;
+                if (col0 >= ncols) break;  // warp-uniform
                 uint32_t acc[32];
                 tc::tmem_ld32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)col0, acc);
 #pragma unroll

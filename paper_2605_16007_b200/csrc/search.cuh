@@ -114,6 +114,7 @@ struct SearchStats {
     float stage_ms[8] = {};
     int64_t pairs = 0;
     int64_t survivors = 0;
+    int64_t max_survivors = 0;
     int retries = 0;
     int launches = 0;
     int used_imma = 0;

@@ -59,7 +59,7 @@ def debug_search(idx, Q, k, nprobe, M, dump=True, **kw):
     )
     if dump:
         cap = nq * nprobe * ((info["max_list"] + 31) // 32) * 32
-        dbg["scan_ip"] = torch.empty(cap, dtype=torch.int32, device=dev)
+        dbg["scan_ip"] = torch.full((cap,), -1, dtype=torch.int32, device=dev)
         dbg["scan_est"] = torch.empty(cap, device=dev)
         dbg["scan_dump_cap"] = cap
     ids, d = idx.search(Q.cuda(), k, nprobe, M, debug=dbg, **kw)
