@@ -12,20 +12,24 @@
 // S back with tcgen05.ld and applies the same estimator + threshold as the
 // popc scan (rabitq_est), so both paths produce bit-identical keys.
 //
-// Work item = (list, 128-vector tile, 128-query group); persistent CTAs
-// stride over the items.  Per item the K loop runs in 128-byte chunks through
-// two shared-memory stages: 256 threads expand codes (A) and cp.async the
-// query rows (B) into the canonical K-major no-swizzle layout while the
-// previous chunk's 4 UMMAs run; tcgen05.commit -> mbarrier frees a stage.
-// 3 CTAs per SM (64 KB of stages each) overlap one CTA's epilogue with
-// another's MMAs.
+// Work item = (list, 128-vector tile, group of <= 256 queries); one
+// persistent CTA per SM strides over the items.  The K loop runs in 128-byte
+// chunks through a 4-stage shared-memory ring: TMA brings the query rows (B,
+// 128-byte swizzle), producer warps expand the code bits (A); a single thread
+// issues the UMMAs into one of two TMEM accumulators (2 x 256 columns) while
+// 8 epilogue warps drain the other (warp-specialised, mbarrier-pipelined).
+// UMMA N is the group size rounded up to 16, so empty columns cost nothing.
 //
 // This ignores query boundaries for scheduling and re-opens the
 // list grouping the paper rejected for its NPU pipeline: on B200 it
 // turns the bandwidth-bound scan into tensor-core work.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <string>
 
 #include "search.cuh"
 #include "tc.cuh"
@@ -33,14 +37,19 @@
 namespace rabitq {
 namespace {
 
-constexpr int kTM = 128;     // vectors per tile (UMMA M)
-constexpr int kTN = 128;     // queries per group (UMMA N)
-constexpr int kKC = 128;     // bytes of K per stage
-constexpr int kNT = 256;     // threads per CTA
-constexpr int kStageA = kTM * kKC;  // 16 KB
-constexpr int kStageB = kTN * kKC;  // 16 KB
-constexpr int kSBO = (kKC / 16) * 128;  // byte distance between 8-row core-matrix groups
-constexpr int kCTAsPerSM = 3;
+constexpr int kTM = 128;                   // vectors per tile (UMMA M)
+constexpr int kTN = 256;                   // queries per group (max UMMA N)
+constexpr int kKC = 128;                   // bytes of K per stage (one 128-byte swizzle row of B)
+constexpr int kStages = 4;
+constexpr int kStageA = kTM * kKC;         // 16 KB, canonical no-swizzle K-major
+constexpr int kStageB = kTN * kKC;         // 32 KB, TMA 128-byte swizzle
+constexpr int kSBO = (kKC / 16) * 128;     // A: distance between 8-row core-matrix groups
+constexpr int kBoxRows = 32;               // TMA box = 32 query rows x 128 bytes
+constexpr int kProdWarps = 4, kEpiWarps = 8;
+constexpr int kMmaWarp = kProdWarps;       // warp 4 issues the UMMAs (and owns TMEM)
+constexpr int kEpiWarp0 = kProdWarps + 1;  // warps 5..12
+constexpr int kNT = (kProdWarps + 1 + kEpiWarps) * 32;  // 416 threads
+constexpr int kTmemCols = 2 * kTN;         // double-buffered accumulator: 512 columns
 
 struct ColC {
     PairC c;        // 16 B
@@ -48,6 +57,12 @@ struct ColC {
     float epsnq;    // eps0 * n_q (lower-bound key)
     int q;          // query (-1: empty column)
     int pair;       // (query, probe) pair index
+};
+
+struct Item {
+    int j;
+    int64_t L, tv, slot0, grow0;
+    int ncols, ncols16, nboxes;
 };
 
 // 16 code bits -> 16 bytes of 0/1 (x * 0x00204081 spreads 4 bits to 4 bytes)
@@ -60,155 +75,194 @@ __device__ __forceinline__ uint4 expand16(uint32_t b) {
     return r;
 }
 
+__device__ __forceinline__ Item decode_item(const ScanArgs& a, int64_t item) {
+    int64_t lo = 0, hi = a.nlist;
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(a.list_items + mid) <= item) lo = mid;
+        else hi = mid;
+    }
+    Item it;
+    it.j = (int)lo;
+    it.L = __ldg(a.list_off + lo + 1) - __ldg(a.list_off + lo);
+    const int64_t gs = __ldg(a.gstart + lo);
+    const int64_t G = __ldg(a.gstart + lo + 1) - gs;
+    const int64_t ng = (G + kTN - 1) / kTN;
+    const int64_t local = item - __ldg(a.list_items + lo);
+    it.tv = local / ng;
+    const int64_t g = local % ng;
+    it.slot0 = __ldg(a.slot_off + lo) + it.tv * kTM;
+    it.grow0 = gs + g * kTN;
+    const int64_t rem = G - g * kTN;
+    it.ncols = (int)(rem < kTN ? rem : kTN);
+    it.ncols16 = (it.ncols + 15) & ~15;
+    it.nboxes = (it.ncols + kBoxRows - 1) / kBoxRows;
+    return it;
+}
+
+// Warp-specialised persistent kernel, one CTA per SM:
+//   warps 0-3  producers: TMA of the query rows (B) + bit -> byte expansion of
+//              the code tile (A) into a 4-stage shared-memory ring
+//   warp 4     MMA issuer: 4 UMMA (K = 32 each) per stage into one of two
+//              TMEM accumulators; tcgen05.commit frees stages / publishes tiles
+//   warps 5-12 epilogue: tcgen05.ld the int32 inner products, fused
+//              estimator (+ bound), threshold, survivor append
 template <bool kLB, bool kDump>
-__global__ __launch_bounds__(kNT, kCTAsPerSM) void scan_imma_kernel(ScanArgs a) {
-    extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t* stA = smem;                       // [2][kStageA]
-    uint8_t* stB = smem + 2 * kStageA;         // [2][kStageB]
-    ColC* colc = reinterpret_cast<ColC*>(smem + 2 * kStageA + 2 * kStageB);  // [kTN]
-    __shared__ __align__(8) uint64_t mbar[2];
+__global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant__ CUtensorMap tmapB, ScanArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    uint8_t* stA = smem;                                   // [kStages][kStageA]
+    uint8_t* stB = smem + kStages * kStageA;               // [kStages][kStageB]
+    ColC* colc = reinterpret_cast<ColC*>(stB + kStages * kStageB);  // [2][kTN]
+    __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], accf_bar[2], acce_bar[2];
     __shared__ uint32_t tmem_base_s;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (warp == 0) tc::tmem_alloc(&tmem_base_s, kTN);
+    if (warp == kMmaWarp) tc::tmem_alloc(&tmem_base_s, kTmemCols);
     if (tid == 0) {
-        tc::mbar_init(&mbar[0], 1);
-        tc::mbar_init(&mbar[1], 1);
+        for (int s = 0; s < kStages; ++s) {
+            tc::mbar_init(&full_bar[s], kProdWarps * 32 + 1);
+            tc::mbar_init(&empty_bar[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&accf_bar[b], 1);
+            tc::mbar_init(&acce_bar[b], kEpiWarps);
+        }
+        tc::prefetch_tmap(&tmapB);
     }
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = tmem_base_s;
-    uint32_t phase[2] = {0u, 0u};
-    bool pending[2] = {false, false};
 
     const int64_t total = a.list_items[a.nlist];
     const int nchunks = (a.Dp + kKC - 1) / kKC;
-    for (int64_t item = blockIdx.x; item < total; item += gridDim.x) {
-        // ---- locate (list, tile, group) ----
-        int64_t lo = 0, hi = a.nlist;
-        while (hi - lo > 1) {
-            const int64_t mid = (lo + hi) >> 1;
-            if (a.list_items[mid] <= item) lo = mid;
-            else hi = mid;
-        }
-        const int j = (int)lo;
-        const int64_t L = a.list_off[j + 1] - a.list_off[j];
-        const int64_t G = a.gstart[j + 1] - a.gstart[j];
-        const int64_t ng = (G + kTN - 1) / kTN;
-        const int64_t local = item - a.list_items[j];
-        const int64_t tv = local / ng, g = local % ng;
-        const int64_t slot0 = a.slot_off[j] + tv * kTM;
-        const int64_t grow0 = a.gstart[j] + g * kTN;
-        const int64_t rem = G - g * kTN;
-        const int ncols = (int)(rem < kTN ? rem : kTN);
-        const int ncols16 = (ncols + 15) & ~15;  // UMMA N (M = 128 needs N % 16 == 0): no MMA work on empty columns
-        const uint32_t idesc = tc::idesc_i8(kTM, ncols16);
 
-        // ---- per-column constants (one query per column) ----
-        if (tid < kTN) {
-            ColC cc;
-            if (tid < ncols) {
-                const int p = a.gpair[grow0 + tid];
-                const int q = p / a.nprobe;
-                cc.c = pair_consts(a.qscal[p], a.D);
-                cc.tau = a.tau[q];
-                cc.epsnq = __fmul_rn(a.eps0, sqrtf(cc.c.nq2));
-                cc.q = q;
-                cc.pair = p;
-            } else {
-                cc.c = PairC{0.f, 0.f, 0.f, 0.f};
-                cc.tau = -INFINITY;
-                cc.epsnq = 0.f;
-                cc.q = -1;
-                cc.pair = -1;
-            }
-            colc[tid] = cc;
-        }
-
-        // ---- K loop: produce stage, issue 4 UMMAs, commit ----
-        for (int c = 0; c < nchunks; ++c) {
-            const int s = c & 1;
-            if (pending[s]) {
-                tc::mbar_wait(&mbar[s], phase[s]);
-                phase[s] ^= 1u;
-                pending[s] = false;
-            }
-            uint8_t* A = stA + s * kStageA;
-            uint8_t* B = stB + s * kStageB;
-            const int kbytes = min(kKC, a.Dp - c * kKC);  // multiple of 32
-            // A: thread -> (row r, 2 code words) -> 4 core-matrix rows of 16 bytes
-            {
-                const int r = tid & (kTM - 1), wp = tid >> 7;
-                const int64_t slot = slot0 + r;
-                const uint32_t* cbase = a.codes + ((size_t)(slot >> 5) * a.W) * 32 + (slot & 31);
+    if (warp < kProdWarps) {
+        // ================= producers =================
+        const int r = tid;  // tile row 0..127 = vector
+        uint32_t gc = 0;    // global chunk counter (stage ring position)
+        for (int64_t item = blockIdx.x; item < total; item += gridDim.x) {
+            const Item it = decode_item(a, item);
+            const int64_t slot = it.slot0 + r;
+            const uint32_t* cbase = a.codes + ((size_t)(slot >> 5) * a.W) * 32 + (slot & 31);
+            uint32_t wnext[4];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int wl = wp * 2 + h;          // word within the chunk
-                    if (wl * 32 >= kbytes) break;
-                    const int w = c * (kKC / 32) + wl;  // < W since kbytes covers it
-                    const uint32_t x = __ldg(cbase + (size_t)w * 32);
-                    uint8_t* dst = A + (r >> 3) * kSBO + (r & 7) * 16 + (wl * 2) * 128;
-                    *reinterpret_cast<uint4*>(dst) = expand16(x & 0xFFFFu);
-                    *reinterpret_cast<uint4*>(dst + 128) = expand16(x >> 16);
+            for (int t = 0; t < 4; ++t) wnext[t] = (t * 32 < min(kKC, a.Dp)) ? __ldg(cbase + (size_t)t * 32) : 0u;
+            for (int c = 0; c < nchunks; ++c, ++gc) {
+                const int s = gc % kStages;
+                const uint32_t u = gc / kStages;
+                const int kbytes = min(kKC, a.Dp - c * kKC);
+                uint32_t wcur[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) wcur[t] = wnext[t];
+                if (c + 1 < nchunks) {  // prefetch the next chunk's code words
+                    const int kb2 = min(kKC, a.Dp - (c + 1) * kKC);
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+                        wnext[t] = (t * 32 < kb2) ? __ldg(cbase + (size_t)((c + 1) * 4 + t) * 32) : 0u;
                 }
-            }
-            // B: the group's query rows (ncols rounded up to 16) x kbytes, 16-byte units by cp.async
-            {
-                const int units = ncols16 * (kbytes / 16);
-                const int per_row = kbytes / 16;
-                for (int u = tid; u < units; u += kNT) {
-                    const int rr = u / per_row, k16 = u % per_row;
-                    const uint8_t* src = a.qbar8 + (size_t)(grow0 + rr) * a.Dp + c * kKC + k16 * 16;
-                    uint8_t* dst = B + (rr >> 3) * kSBO + (rr & 7) * 16 + k16 * 128;
-                    tc::cp_async16(dst, src);
+                if (u > 0) tc::mbar_wait(&empty_bar[s], (u - 1) & 1);
+                if (tid == 0) {
+                    tc::mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(it.nboxes * kBoxRows * kKC));
+                    for (int bx = 0; bx < it.nboxes; ++bx)
+                        tc::tma_load_2d(stB + s * kStageB + bx * kBoxRows * kKC, &tmapB, &full_bar[s], c * kKC,
+                                        (int)(it.grow0 + bx * kBoxRows));
                 }
+                uint8_t* A = stA + s * kStageA + (r >> 3) * kSBO + (r & 7) * 16;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    if (t * 32 >= kbytes) break;
+                    *reinterpret_cast<uint4*>(A + (2 * t) * 128) = expand16(wcur[t] & 0xFFFFu);
+                    *reinterpret_cast<uint4*>(A + (2 * t + 1) * 128) = expand16(wcur[t] >> 16);
+                }
+                tc::fence_proxy_async();
+                tc::mbar_arrive(&full_bar[s]);
             }
-            tc::cp_async_wait_all();
-            tc::fence_proxy_async();
-            __syncthreads();
-            if (tid == 0) {
+        }
+    } else if (warp == kMmaWarp) {
+        // ================= MMA issuer =================
+        uint32_t gc = 0, ic = 0;
+        for (int64_t item = blockIdx.x; item < total; item += gridDim.x, ++ic) {
+            const Item it = decode_item(a, item);
+            const uint32_t idesc = tc::idesc_i8(kTM, it.ncols16);
+            const int b = ic & 1;
+            const uint32_t ub = ic >> 1;
+            if (ub > 0) tc::mbar_wait(&acce_bar[b], (ub - 1) & 1);
+            tc::fence_after_sync();
+            const uint32_t dacc = tmem + (uint32_t)(b * kTN);
+            for (int c = 0; c < nchunks; ++c, ++gc) {
+                const int s = gc % kStages;
+                const uint32_t u = gc / kStages;
+                const int kbytes = min(kKC, a.Dp - c * kKC);
+                tc::mbar_wait(&full_bar[s], u & 1);
                 tc::fence_after_sync();
-                const uint32_t aaddr = tc::smem_u32(A), baddr = tc::smem_u32(B);
-                for (int ks = 0; ks < kbytes / 32; ++ks) {
-                    const uint64_t ad = tc::smem_desc(aaddr + ks * 256, 128, kSBO);
-                    const uint64_t bd = tc::smem_desc(baddr + ks * 256, 128, kSBO);
-                    tc::mma_i8(tmem, ad, bd, idesc, (c > 0 || ks > 0) ? 1u : 0u);
+                if (lane == 0) {
+                    const uint32_t aaddr = tc::smem_u32(stA + s * kStageA), baddr = tc::smem_u32(stB + s * kStageB);
+                    for (int ks = 0; ks < kbytes / 32; ++ks) {
+                        const uint64_t ad = tc::smem_desc(aaddr + ks * 256, 128, kSBO);
+                        const uint64_t bd = tc::smem_desc_sw128(baddr + ks * 32);
+                        tc::mma_i8(dacc, ad, bd, idesc, (c > 0 || ks > 0) ? 1u : 0u);
+                    }
+                    tc::commit(&empty_bar[s]);                       // stage s free once these UMMAs retire
+                    if (c == nchunks - 1) tc::commit(&accf_bar[b]);  // accumulator b complete
                 }
-                tc::commit(&mbar[s]);
+                __syncwarp();
             }
-            pending[s] = true;
         }
-        // all UMMAs of this item done <=> the last commit arrived
-        {
-            const int s = (nchunks - 1) & 1;
-            tc::mbar_wait(&mbar[s], phase[s]);
-            phase[s] ^= 1u;
-            pending[s] = false;
-        }
-        tc::fence_after_sync();
-
-        // ---- epilogue: S from TMEM -> estimator -> threshold -> append ----
-        {
-            const int r = (warp & 3) * 32 + lane;  // TMEM lane = tile row = vector
-            const int64_t v = tv * kTM + r;
-            const bool vok = v < L;
-            const int64_t slot = slot0 + r;
+    } else {
+        // ================= epilogue =================
+        const int e = warp - kEpiWarp0;     // 0..7
+        const int quarter = warp & 3;       // TMEM lanes this warp may access: 32 * (warp % 4) ..
+        const int half = e >> 2;            // column half
+        const int r = quarter * 32 + lane;  // tile row = vector
+        const int et = e * 32 + lane;       // 0..255 among epilogue threads
+        uint32_t ic = 0;
+        for (int64_t item = blockIdx.x; item < total; item += gridDim.x, ++ic) {
+            const Item it = decode_item(a, item);
+            const int b = ic & 1;
+            const uint32_t ub = ic >> 1;
+            ColC* cb = colc + b * kTN;
+            tc::named_barrier(1, kEpiWarps * 32);  // every epilogue warp is done with this buffer's last item
+            {
+                ColC cc;
+                if (et < it.ncols) {
+                    const int p = a.gpair[it.grow0 + et];
+                    const int q = p / a.nprobe;
+                    cc.c = pair_consts(a.qscal[p], a.D);
+                    cc.tau = a.tau[q];
+                    cc.epsnq = __fmul_rn(a.eps0, sqrtf(cc.c.nq2));
+                    cc.q = q;
+                    cc.pair = p;
+                } else {
+                    cc.c = PairC{0.f, 0.f, 0.f, 0.f};
+                    cc.tau = -INFINITY;
+                    cc.epsnq = 0.f;
+                    cc.q = -1;
+                    cc.pair = -1;
+                }
+                cb[et] = cc;
+            }
+            const int64_t v = it.tv * kTM + r;
+            const bool vok = v < it.L;
+            const int64_t slot = it.slot0 + r;
             const float2 fac = vok ? a.fac[slot] : make_float2(0.f, 0.f);
             const int pc = vok ? (int)a.pcnt[slot] : 0;
             const float g1 = (kLB && vok) ? a.g1[slot] : 0.f;
-            const int colbase = (warp >> 2) * 64;
+            tc::named_barrier(1, kEpiWarps * 32);  // column constants written
+            tc::mbar_wait(&accf_bar[b], ub & 1);
+            tc::fence_after_sync();
 #pragma unroll 1
-            for (int h = 0; h < 2; ++h) {
-                const int col0 = colbase + h * 32;
-                if (col0 >= ncols) break;  // warp-uniform
+            for (int h = 0; h < kTN / 64; ++h) {
+                const int col0 = half * (kTN / 2) + h * 32;
+                if (col0 >= it.ncols) break;  // warp-uniform
                 uint32_t acc[32];
-                tc::tmem_ld32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)col0, acc);
+                tc::tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * kTN + col0), acc);
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
                     const int cidx = col0 + i;
-                    if (cidx >= ncols) break;  // warp-uniform
-                    const ColC& cc = colc[cidx];
+                    if (cidx >= it.ncols) break;  // warp-uniform
+                    const ColC& cc = cb[cidx];
                     const int ip = (int)acc[i];
                     const float est = rabitq_est(ip, pc, fac, cc.c);
                     const float key = rank_key<kLB>(est, cc.epsnq, g1);
@@ -234,16 +288,14 @@ __global__ __launch_bounds__(kNT, kCTAsPerSM) void scan_imma_kernel(ScanArgs a) 
                     }
                 }
             }
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&acce_bar[b]);  // accumulator b may be overwritten
         }
-        tc::fence_before_sync();
-        __syncthreads();  // TMEM accumulator and colc are free for the next item
     }
-    // drain: a stage may still have an outstanding commit
-    for (int s = 0; s < 2; ++s)
-        if (pending[s]) tc::mbar_wait(&mbar[s], phase[s]);
     tc::fence_before_sync();
     __syncthreads();
-    if (warp == 0) tc::tmem_dealloc(tmem, kTN);
+    if (warp == kMmaWarp) tc::tmem_dealloc(tmem, kTmemCols);
 }
 
 // ------------------------------------------------------------ list grouping
@@ -318,17 +370,39 @@ void prepare_groups(const rabitq_index* idx, const int32_t* probes, int64_t npai
     launches += 7;
 }
 
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        RQ_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        RQ_REQUIRE(p && q == cudaDriverEntryPointSuccess, RABITQ_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
 void scan_imma(const ScanArgs& a, bool lb, bool dump, cudaStream_t st) {
     int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const size_t smem = 2 * (size_t)kStageA + 2 * (size_t)kStageB + kTN * sizeof(ColC);
-    const int grid = sms * kCTAsPerSM;
-#define RQ_IMMA(LB, DP)                                                                              \
-    do {                                                                                             \
+    RQ_CUDA(cudaGetDevice(&dev));
+    RQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    // B = grouped int8 query rows [(npairs + kTN) x Dp]; TMA box 128 bytes x 32 rows, 128-byte swizzle
+    CUtensorMap tmap;
+    const cuuint64_t gdim[2] = {(cuuint64_t)a.Dp, (cuuint64_t)(a.npairs + kTN)};
+    const cuuint64_t gstride[1] = {(cuuint64_t)a.Dp};
+    const cuuint32_t box[2] = {(cuuint32_t)kKC, (cuuint32_t)kBoxRows};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult cr = get_encode()(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(a.qbar8), gdim, gstride,
+                               box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    RQ_REQUIRE(cr == CUDA_SUCCESS, RABITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
+    const size_t smem = 1024 + (size_t)kStages * (kStageA + kStageB) + 2 * kTN * sizeof(ColC);
+    const int grid = sms;
+#define RQ_IMMA(LB, DP)                                                                                     \
+    do {                                                                                                    \
         RQ_CUDA(cudaFuncSetAttribute(scan_imma_kernel<LB, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                     (int)smem));                                                    \
-        scan_imma_kernel<LB, DP><<<grid, kNT, smem, st>>>(a);                                        \
+                                     (int)smem));                                                           \
+        scan_imma_kernel<LB, DP><<<grid, kNT, smem, st>>>(tmap, a);                                         \
     } while (0)
     if (dump) {
         if (lb) RQ_IMMA(true, true);
