@@ -51,13 +51,6 @@ constexpr int kEpiWarp0 = kProdWarps + 1;  // warps 5..12
 constexpr int kNT = (kProdWarps + 1 + kEpiWarps) * 32;  // 416 threads
 constexpr int kTmemCols = 2 * kTN;         // double-buffered accumulator: 512 columns
 
-struct ColC {
-    PairC c;        // 16 B
-    float tau;      // threshold of the column's query
-    float epsnq;    // eps0 * n_q (lower-bound key)
-    int q;          // query (-1: empty column)
-    int pair;       // (query, probe) pair index
-};
 
 struct Item {
     int j;
@@ -113,7 +106,7 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     uint8_t* stA = smem;                                   // [kStages][kStageA]
     uint8_t* stB = smem + kStages * kStageA;               // [kStages][kStageB]
-    ColC* colc = reinterpret_cast<ColC*>(stB + kStages * kStageB);  // [2][kTN]
+    __shared__ __align__(16) ColC colc[2 * kTN];
     __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], accf_bar[2], acce_bar[2];
     __shared__ uint32_t tmem_base_s;
 
@@ -218,30 +211,36 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
         const int r = quarter * 32 + lane;  // tile row = vector
         const int et = e * 32 + lane;       // 0..255 among epilogue threads
         uint32_t ic = 0;
-        for (int64_t item = blockIdx.x; item < total; item += gridDim.x, ++ic) {
-            const Item it = decode_item(a, item);
+        int64_t item = blockIdx.x;
+        Item it{};
+        ColC nextc;
+        auto fetch_colc = [&](const Item& x) {  // one coalesced 32-byte load per column
+            if (et < x.ncols) {
+                nextc = a.gcolc[x.grow0 + et];
+            } else {
+                nextc.c = PairC{0.f, 0.f, 0.f, 0.f};
+                nextc.tau = -INFINITY;
+                nextc.epsnq = 0.f;
+                nextc.q = -1;
+                nextc.pair = -1;
+            }
+        };
+        if (item < total) {
+            it = decode_item(a, item);
+            fetch_colc(it);
+            colc[et] = nextc;
+        }
+        tc::named_barrier(1, kEpiWarps * 32);
+        for (; item < total; item += gridDim.x, ++ic) {
             const int b = ic & 1;
             const uint32_t ub = ic >> 1;
-            ColC* cb = colc + b * kTN;
-            tc::named_barrier(1, kEpiWarps * 32);  // every epilogue warp is done with this buffer's last item
-            {
-                ColC cc;
-                if (et < it.ncols) {
-                    const int p = a.gpair[it.grow0 + et];
-                    const int q = p / a.nprobe;
-                    cc.c = pair_consts(a.qscal[p], a.D);
-                    cc.tau = a.tau[q];
-                    cc.epsnq = __fmul_rn(a.eps0, sqrtf(cc.c.nq2));
-                    cc.q = q;
-                    cc.pair = p;
-                } else {
-                    cc.c = PairC{0.f, 0.f, 0.f, 0.f};
-                    cc.tau = -INFINITY;
-                    cc.epsnq = 0.f;
-                    cc.q = -1;
-                    cc.pair = -1;
-                }
-                cb[et] = cc;
+            const ColC* cb = colc + b * kTN;
+            // prefetch the next item's column constants (latency hidden by this item)
+            const int64_t nitem = item + gridDim.x;
+            Item nit{};
+            if (nitem < total) {
+                nit = decode_item(a, nitem);
+                fetch_colc(nit);
             }
             const int64_t v = it.tv * kTM + r;
             const bool vok = v < it.L;
@@ -249,7 +248,7 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
             const float2 fac = vok ? a.fac[slot] : make_float2(0.f, 0.f);
             const int pc = vok ? (int)a.pcnt[slot] : 0;
             const float g1 = (kLB && vok) ? a.g1[slot] : 0.f;
-            tc::named_barrier(1, kEpiWarps * 32);  // column constants written
+            const uint32_t row = vok ? a.rows[slot] : 0u;
             tc::mbar_wait(&accf_bar[b], ub & 1);
             tc::fence_after_sync();
 #pragma unroll 1
@@ -258,16 +257,17 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                 if (col0 >= it.ncols) break;  // warp-uniform
                 uint32_t acc[32];
                 tc::tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * kTN + col0), acc);
+                // phase 1: keys + survivor ballots of 32 columns; lane i keeps column i's ballot
+                float key[32];
+                uint32_t myballot = 0u;
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
-                    const int cidx = col0 + i;
-                    if (cidx >= it.ncols) break;  // warp-uniform
-                    const ColC& cc = cb[cidx];
+                    const ColC& cc = cb[col0 + i];  // empty columns have tau = -inf
                     const int ip = (int)acc[i];
                     const float est = rabitq_est(ip, pc, fac, cc.c);
-                    const float key = rank_key<kLB>(est, cc.epsnq, g1);
+                    key[i] = rank_key<kLB>(est, cc.epsnq, g1);
                     if constexpr (kDump) {
-                        if (vok) {
+                        if (vok && col0 + i < it.ncols) {
                             const int64_t di = (a.item_off[cc.pair] + (v >> 5)) * 32 + (v & 31);
                             if (di < a.dump_cap) {
                                 a.dump_ip[di] = ip;
@@ -275,15 +275,22 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                             }
                         }
                     }
-                    const bool surv = vok && key <= cc.tau;
-                    const uint32_t ballot = __ballot_sync(0xFFFFFFFFu, surv);
-                    if (ballot) {
-                        int base = 0;
-                        if (lane == 0) base = atomicAdd(&a.cnt[cc.q], __popc(ballot));
-                        base = __shfl_sync(0xFFFFFFFFu, base, 0);
-                        if (surv) {
-                            const int pos = base + __popc(ballot & ((1u << lane) - 1u));
-                            if (pos < a.cap) a.buf[(size_t)cc.q * a.cap + pos] = make_key(key, a.rows[slot]);
+                    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, vok && key[i] <= cc.tau);
+                    if (lane == i) myballot = bal;
+                }
+                // phase 2: one atomic per surviving column, all issued together by their lanes
+                const uint32_t cols = __ballot_sync(0xFFFFFFFFu, myballot != 0u);
+                if (cols) {
+                    int mybase = 0;
+                    if (myballot) mybase = atomicAdd(&a.cnt[cb[col0 + lane].q], __popc(myballot));
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        if (!(cols >> i & 1u)) continue;  // warp-uniform
+                        const uint32_t bal = __shfl_sync(0xFFFFFFFFu, myballot, i);
+                        const int base = __shfl_sync(0xFFFFFFFFu, mybase, i);
+                        if (bal >> lane & 1u) {
+                            const int pos = base + __popc(bal & ((1u << lane) - 1u));
+                            if (pos < a.cap) a.buf[(size_t)cb[col0 + i].q * a.cap + pos] = make_key(key[i], row);
                         }
                     }
                 }
@@ -291,6 +298,11 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
             tc::fence_before_sync();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&acce_bar[b]);  // accumulator b may be overwritten
+            // publish the next item's column constants into the other buffer (its last
+            // readers finished item ic - 1 before the previous barrier)
+            if (nitem < total) colc[(b ^ 1) * kTN + et] = nextc;
+            tc::named_barrier(1, kEpiWarps * 32);
+            it = nit;
         }
     }
     tc::fence_before_sync();
@@ -312,6 +324,23 @@ __global__ void group_fill_kernel(const int32_t* __restrict__ probes, int64_t np
         const int64_t pos = gstart[j] + atomicAdd(&gfill[j], 1);
         gpos[p] = (int32_t)pos;
         gpair[pos] = (int32_t)p;
+    }
+}
+
+// column constants of every grouped row (one 32-byte record per (query, list) pair)
+__global__ void colc_kernel(const int32_t* __restrict__ gpair, int64_t npairs, int nprobe, int D,
+                            const float4* __restrict__ qscal, const float* __restrict__ tau, float eps0,
+                            ColC* __restrict__ gcolc) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < npairs; g += (int64_t)gridDim.x * blockDim.x) {
+        const int p = gpair[g];
+        const int q = p / nprobe;
+        ColC cc;
+        cc.c = pair_consts(qscal[p], D);
+        cc.tau = tau[q];
+        cc.epsnq = __fmul_rn(eps0, sqrtf(cc.c.nq2));
+        cc.q = q;
+        cc.pair = p;
+        gcolc[g] = cc;
     }
 }
 
@@ -382,7 +411,14 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-void scan_imma(const ScanArgs& a, bool lb, bool dump, cudaStream_t st) {
+void scan_imma(const ScanArgs& a_in, bool lb, bool dump, cudaStream_t st) {
+    ScanArgs a = a_in;
+    WBuf<ColC> gcolc;
+    gcolc.alloc((size_t)a.npairs + kTN, st);
+    colc_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((a.npairs + 255) / 256, 2048)), 256, 0, st>>>(
+        a.gpair, a.npairs, a.nprobe, a.D, a.qscal, a.tau, a.eps0, gcolc.p);
+    RQ_CHECK_LAUNCH();
+    a.gcolc = gcolc.p;
     int dev = 0, sms = 148;
     RQ_CUDA(cudaGetDevice(&dev));
     RQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -396,7 +432,7 @@ void scan_imma(const ScanArgs& a, bool lb, bool dump, cudaStream_t st) {
                                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     RQ_REQUIRE(cr == CUDA_SUCCESS, RABITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
-    const size_t smem = 1024 + (size_t)kStages * (kStageA + kStageB) + 2 * kTN * sizeof(ColC);
+    const size_t smem = 1024 + (size_t)kStages * (kStageA + kStageB);
     const int grid = sms;
 #define RQ_IMMA(LB, DP)                                                                                     \
     do {                                                                                                    \

@@ -5,6 +5,14 @@
 
 namespace rabitq {
 
+struct ColC {      // per grouped row (query, list) constants of the grouped scan epilogue
+    PairC c;       // 16 B
+    float tau;     // threshold of the column's query
+    float epsnq;   // eps0 * n_q (lower-bound key)
+    int q;         // query (-1: empty column)
+    int pair;      // (query, probe) pair index
+};
+
 struct ScanArgs {
     const int32_t* probes;     // [npairs] list of each (q, probe) pair
     int64_t npairs;
@@ -37,6 +45,7 @@ struct ScanArgs {
     const uint8_t* qbar8;      // [(npairs + 128) x Dp] quantized queries, grouped by list
     const int64_t* list_items; // [nlist + 1] prefix of (128-vector tile, 128-query group) items
     const uint16_t* pcnt;      // [nslots] popcount of each code
+    const ColC* gcolc;         // [npairs] column constants in grouped order
 };
 
 template <typename T>
