@@ -100,7 +100,7 @@ __device__ __forceinline__ Item decode_item(const ScanArgs& a, int64_t item) {
 //              TMEM accumulators; tcgen05.commit frees stages / publishes tiles
 //   warps 5-12 epilogue: tcgen05.ld the int32 inner products, fused
 //              estimator (+ bound), threshold, survivor append
-template <bool kLB, bool kDump>
+template <bool kLB, bool kDump, bool kRetry>
 __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant__ CUtensorMap tmapB, ScanArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -275,7 +275,14 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                             }
                         }
                     }
-                    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, vok && key[i] <= cc.tau);
+                    bool sv;
+                    if constexpr (kRetry) {  // exact (key, row) <= tau64 (overflow re-scan)
+                        const uint32_t ko = f2o(key[i]), to = f2o(cc.tau);
+                        sv = vok && (ko < to || (ko == to && row <= (uint32_t)cc.pair));
+                    } else {
+                        sv = vok && key[i] <= cc.tau;
+                    }
+                    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, sv);
                     if (lane == i) myballot = bal;
                 }
                 // phase 2: one atomic per surviving column, all issued together by their lanes
@@ -311,35 +318,64 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
 }
 
 // ------------------------------------------------------------ list grouping
-__global__ void group_count_kernel(const int32_t* __restrict__ probes, int64_t npairs, int64_t* __restrict__ gcount) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npairs; p += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd((unsigned long long*)&gcount[probes[p]], 1ull);
+// pairs to group: all (sub == nullptr) or the listed pair indices
+__global__ void group_count_kernel(const int32_t* __restrict__ probes, const int32_t* __restrict__ sub, int64_t n,
+                                   int64_t* __restrict__ gcount) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd((unsigned long long*)&gcount[probes[sub ? sub[i] : i]], 1ull);
 }
 
-__global__ void group_fill_kernel(const int32_t* __restrict__ probes, int64_t npairs,
+__global__ void group_fill_kernel(const int32_t* __restrict__ probes, const int32_t* __restrict__ sub, int64_t n,
                                   const int64_t* __restrict__ gstart, int32_t* __restrict__ gfill,
                                   int32_t* __restrict__ gpos, int32_t* __restrict__ gpair) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npairs; p += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int p = sub ? sub[i] : (int)i;
         const int j = probes[p];
         const int64_t pos = gstart[j] + atomicAdd(&gfill[j], 1);
-        gpos[p] = (int32_t)pos;
+        gpos[i] = (int32_t)pos;
         gpair[pos] = (int32_t)p;
     }
 }
 
+// copy the int8 query rows of the listed pairs from the full grouping into a sub grouping
+__global__ void gather_rows_kernel(const int32_t* __restrict__ sub, int64_t n, const int32_t* __restrict__ gpos_full,
+                                   const uint8_t* __restrict__ q8_full, const int32_t* __restrict__ gpos_sub,
+                                   uint8_t* __restrict__ q8_sub, int Dp) {
+    const int per = Dp / 16;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * per; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / per;
+        const int k = (int)(e % per);
+        const uint4 v = reinterpret_cast<const uint4*>(q8_full + (size_t)gpos_full[sub[i]] * Dp)[k];
+        reinterpret_cast<uint4*>(q8_sub + (size_t)gpos_sub[i] * Dp)[k] = v;
+    }
+}
+
+// pairs of the flagged (overflowed) queries
+__global__ void compact_flagged_kernel(const int* __restrict__ flags, int64_t npairs, int nprobe,
+                                       int32_t* __restrict__ sub, int* __restrict__ n) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npairs; p += (int64_t)gridDim.x * blockDim.x)
+        if (flags[p / nprobe]) sub[atomicAdd(n, 1)] = (int32_t)p;
+}
+
 // column constants of every grouped row (one 32-byte record per (query, list) pair)
+// (re-scan: tau / pair carry the 64-bit (key, row) threshold instead)
 __global__ void colc_kernel(const int32_t* __restrict__ gpair, int64_t npairs, int nprobe, int D,
-                            const float4* __restrict__ qscal, const float* __restrict__ tau, float eps0,
-                            ColC* __restrict__ gcolc) {
+                            const float4* __restrict__ qscal, const float* __restrict__ tau,
+                            const uint64_t* __restrict__ tau64, float eps0, ColC* __restrict__ gcolc) {
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < npairs; g += (int64_t)gridDim.x * blockDim.x) {
         const int p = gpair[g];
         const int q = p / nprobe;
         ColC cc;
         cc.c = pair_consts(qscal[p], D);
-        cc.tau = tau[q];
         cc.epsnq = __fmul_rn(eps0, sqrtf(cc.c.nq2));
         cc.q = q;
-        cc.pair = p;
+        if (tau64) {
+            cc.tau = o2f((uint32_t)(tau64[q] >> 32));
+            cc.pair = (int)(uint32_t)tau64[q];
+        } else {
+            cc.tau = tau[q];
+            cc.pair = p;
+        }
         gcolc[g] = cc;
     }
 }
@@ -366,23 +402,24 @@ bool imma_wanted(const rabitq_index* idx, int64_t npairs, int scan_path) {
     return npairs >= (int64_t)8 * idx->nlist;
 }
 
-void prepare_groups(const rabitq_index* idx, const int32_t* probes, int64_t npairs, Groups& g, cudaStream_t st,
-                    int& launches) {
+void prepare_groups(const rabitq_index* idx, const int32_t* probes, int64_t n, const int32_t* sub, Groups& g,
+                    cudaStream_t st, int& launches) {
     const int nlist = idx->nlist;
     g.Dp = ((idx->D + 31) / 32) * 32;
+    g.n = n;
     g.gcount.alloc((size_t)nlist + 1, st);
     g.gstart.alloc((size_t)nlist + 1, st);
     g.itemc.alloc((size_t)nlist + 1, st);
     g.list_items.alloc((size_t)nlist + 1, st);
     g.gfill.alloc((size_t)nlist, st);
-    g.gpos.alloc((size_t)npairs, st);
-    g.gpair.alloc((size_t)npairs + kTN, st);
-    g.qbar8.alloc(((size_t)npairs + kTN) * g.Dp, st);
+    g.gpos.alloc((size_t)n, st);
+    g.gpair.alloc((size_t)n + kTN, st);
+    g.qbar8.alloc(((size_t)n + kTN) * g.Dp, st);
     RQ_CUDA(cudaMemsetAsync(g.gcount.p, 0, ((size_t)nlist + 1) * sizeof(int64_t), st));
     RQ_CUDA(cudaMemsetAsync(g.gfill.p, 0, (size_t)nlist * sizeof(int32_t), st));
-    RQ_CUDA(cudaMemsetAsync(g.gpair.p + npairs, 0, kTN * sizeof(int32_t), st));
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((npairs + 255) / 256, 2048));
-    group_count_kernel<<<grid, 256, 0, st>>>(probes, npairs, g.gcount.p);
+    RQ_CUDA(cudaMemsetAsync(g.gpair.p + n, 0, kTN * sizeof(int32_t), st));
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 2048));
+    group_count_kernel<<<grid, 256, 0, st>>>(probes, sub, n, g.gcount.p);
     RQ_CHECK_LAUNCH();
     size_t tb = 0;
     RQ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, g.gcount.p, g.gstart.p, nlist + 1, st));
@@ -391,12 +428,35 @@ void prepare_groups(const rabitq_index* idx, const int32_t* probes, int64_t npai
     WBuf<uint8_t> tmp;
     tmp.alloc(std::max(tb, tb2), st);
     RQ_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, g.gcount.p, g.gstart.p, nlist + 1, st));
-    group_fill_kernel<<<grid, 256, 0, st>>>(probes, npairs, g.gstart.p, g.gfill.p, g.gpos.p, g.gpair.p);
+    group_fill_kernel<<<grid, 256, 0, st>>>(probes, sub, n, g.gstart.p, g.gfill.p, g.gpos.p, g.gpair.p);
     RQ_CHECK_LAUNCH();
     list_items_kernel<<<(nlist + 256) / 256, 256, 0, st>>>(nlist, idx->list_off, g.gcount.p, g.itemc.p);
     RQ_CHECK_LAUNCH();
     RQ_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb2, g.itemc.p, g.list_items.p, nlist + 1, st));
     launches += 7;
+}
+
+int64_t regroup_flagged(const rabitq_index* idx, const int32_t* probes, int64_t npairs, int nprobe, const int* flags,
+                        const Groups& full, Groups& sub, cudaStream_t st, int& launches) {
+    WBuf<int32_t> list;
+    list.alloc((size_t)npairs, st);
+    WBuf<int> cnt;
+    cnt.alloc(1, st);
+    RQ_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int), st));
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((npairs + 255) / 256, 2048));
+    compact_flagged_kernel<<<grid, 256, 0, st>>>(flags, npairs, nprobe, list.p, cnt.p);
+    RQ_CHECK_LAUNCH();
+    int n = 0;
+    RQ_CUDA(cudaMemcpyAsync(&n, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    RQ_CUDA(cudaStreamSynchronize(st));
+    if (n == 0) return 0;
+    prepare_groups(idx, probes, n, list.p, sub, st, launches);
+    const int per = full.Dp / 16;
+    gather_rows_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(((int64_t)n * per + 255) / 256, 4096)), 256,
+                         0, st>>>(list.p, n, full.gpos.p, full.qbar8.p, sub.gpos.p, sub.qbar8.p, full.Dp);
+    RQ_CHECK_LAUNCH();
+    launches += 2;
+    return n;
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -411,12 +471,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-void scan_imma(const ScanArgs& a_in, bool lb, bool dump, cudaStream_t st) {
-    ScanArgs a = a_in;
+void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_t st) {
+    ScanArgs a = a_in;  // a.npairs = grouped rows (all pairs, or the re-scan's sub list)
     WBuf<ColC> gcolc;
     gcolc.alloc((size_t)a.npairs + kTN, st);
     colc_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((a.npairs + 255) / 256, 2048)), 256, 0, st>>>(
-        a.gpair, a.npairs, a.nprobe, a.D, a.qscal, a.tau, a.eps0, gcolc.p);
+        a.gpair, a.npairs, a.nprobe, a.D, a.qscal, a.tau, retry ? a.tau64 : nullptr, a.eps0, gcolc.p);
     RQ_CHECK_LAUNCH();
     a.gcolc = gcolc.p;
     int dev = 0, sms = 148;
@@ -434,18 +494,21 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, cudaStream_t st) {
     RQ_REQUIRE(cr == CUDA_SUCCESS, RABITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
     const size_t smem = 1024 + (size_t)kStages * (kStageA + kStageB);
     const int grid = sms;
-#define RQ_IMMA(LB, DP)                                                                                     \
-    do {                                                                                                    \
-        RQ_CUDA(cudaFuncSetAttribute(scan_imma_kernel<LB, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                     (int)smem));                                                           \
-        scan_imma_kernel<LB, DP><<<grid, kNT, smem, st>>>(tmap, a);                                         \
+#define RQ_IMMA(LB, DP, RT)                                                                                     \
+    do {                                                                                                        \
+        RQ_CUDA(cudaFuncSetAttribute(scan_imma_kernel<LB, DP, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                     (int)smem));                                                               \
+        scan_imma_kernel<LB, DP, RT><<<grid, kNT, smem, st>>>(tmap, a);                                         \
     } while (0)
     if (dump) {
-        if (lb) RQ_IMMA(true, true);
-        else RQ_IMMA(false, true);
+        if (lb) RQ_IMMA(true, true, false);
+        else RQ_IMMA(false, true, false);
+    } else if (retry) {
+        if (lb) RQ_IMMA(true, false, true);
+        else RQ_IMMA(false, false, true);
     } else {
-        if (lb) RQ_IMMA(true, false);
-        else RQ_IMMA(false, false);
+        if (lb) RQ_IMMA(true, false, false);
+        else RQ_IMMA(false, false, false);
     }
 #undef RQ_IMMA
     RQ_CHECK_LAUNCH();

@@ -67,9 +67,12 @@ struct Groups {
     WBuf<int32_t> gfill, gpos, gpair;
     WBuf<uint8_t> qbar8;
     int Dp = 0;
+    int64_t n = 0;  // grouped rows
 };
-void prepare_groups(const rabitq_index* idx, const int32_t* probes, int64_t npairs, Groups& g, cudaStream_t st,
-                    int& launches);
+void prepare_groups(const rabitq_index* idx, const int32_t* probes, int64_t n, const int32_t* sub, Groups& g,
+                    cudaStream_t st, int& launches);
+int64_t regroup_flagged(const rabitq_index* idx, const int32_t* probes, int64_t npairs, int nprobe, const int* flags,
+                        const Groups& full, Groups& sub, cudaStream_t st, int& launches);
 bool imma_wanted(const rabitq_index* idx, int64_t npairs, int scan_path);
 
 struct RerankArgs {
@@ -133,7 +136,7 @@ struct SearchStats {
 void search_batch(const rabitq_index* idx, const float* Q, int64_t nq, int k, int nprobe, int M,
                   const SearchCfg& cfg, int64_t qid_base, int64_t* ids, float* dists, const DebugOut& dbg,
                   cudaStream_t st, SearchStats* stats);
-void scan_imma(const ScanArgs& a, bool lb, bool dump, cudaStream_t st);
+void scan_imma(const ScanArgs& a, bool lb, bool dump, bool retry, cudaStream_t st);
 void scan_popc_entry(const ScanArgs& a, bool lb, bool retry, bool dump, cudaStream_t st);
 void merge_topk(const int64_t* in_ids, const float* in_d, int G, int64_t nq, int k, int64_t* out_ids,
                 float* out_d, cudaStream_t st);
