@@ -270,6 +270,11 @@ def test_invariances(orc):
     assert int(retries.item()) >= 1  # the overflow path ran
     s_i, s_d = idx.search(Qd, 10, 8, 100, seed_max=100)
     assert torch.equal(s_i, base_i) and torch.equal(s_d, base_d)
+    # the tensor-core scan and its regrouped overflow re-scan give the same answer
+    r2 = torch.zeros(1, dtype=torch.int32, device="cuda")
+    t_i, t_d = idx.search(Qd, 10, 8, 100, cap=200, seed_max=100, scan_path=rq.SCAN_IMMA, debug=dict(retries=r2))
+    assert torch.equal(t_i, base_i) and torch.equal(t_d, base_d)
+    assert int(r2.item()) >= 1
 
 
 def test_edge_cases():
