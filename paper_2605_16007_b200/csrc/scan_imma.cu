@@ -50,7 +50,6 @@ constexpr int kMmaWarp = kProdWarps;       // warp 4 issues the UMMAs (and owns 
 constexpr int kEpiWarp0 = kProdWarps + 1;  // warps 5..12
 constexpr int kNT = (kProdWarps + 1 + kEpiWarps) * 32;  // 416 threads
 constexpr int kTmemCols = 2 * kTN;         // double-buffered accumulator: 512 columns
-constexpr int kScratch = 4 * 32 * 32;      // survivor staging entries per (warp, list): every pair of an item
 
 
 struct Item {
@@ -108,7 +107,6 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
     uint8_t* stA = smem;                                   // [kStages][kStageA]
     uint8_t* stB = smem + kStages * kStageA;               // [kStages][kStageB]
     __shared__ __align__(16) ColC colc[2 * kTN];
-    __shared__ int ebase[kEpiWarps][4 * 32];
     __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], accf_bar[2], acce_bar[2];
     __shared__ uint32_t tmem_base_s;
 
@@ -194,7 +192,8 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                 tc::fence_after_sync();
                 if (lane == 0) {
                     const uint32_t aaddr = tc::smem_u32(stA + s * kStageA), baddr = tc::smem_u32(stB + s * kStageB);
-                    for (int ks = 0; ks < kbytes / 32; ++ks) {
+                    const int nks = (a.experiment & 2) ? ((c == 0) ? 1 : 0) : kbytes / 32;
+                    for (int ks = 0; ks < nks; ++ks) {
                         const uint64_t ad = tc::smem_desc(aaddr + ks * 256, 128, kSBO);
                         const uint64_t bd = tc::smem_desc_sw128(baddr + ks * 32);
                         tc::mma_i8(dacc, ad, bd, idesc, (c > 0 || ks > 0) ? 1u : 0u);
@@ -207,19 +206,11 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
         }
     } else {
         // ================= epilogue =================
-        // Survivors are staged per warp in a global scratch list and committed one
-        // item later: the per-column atomicAdds that reserve buffer space are all
-        // issued together at the end of an item and their results consumed only
-        // after the next item's compute, so no warp waits on an atomic round trip.
         const int e = warp - kEpiWarp0;     // 0..7
         const int quarter = warp & 3;       // TMEM lanes this warp may access: 32 * (warp % 4) ..
         const int half = e >> 2;            // column half
         const int r = quarter * 32 + lane;  // tile row = vector
         const int et = e * 32 + lane;       // 0..255 among epilogue threads
-        const int64_t gw = (int64_t)blockIdx.x * kEpiWarps + e;
-        uint64_t* sval[2] = {a.scratch_val + (gw * 2 + 0) * kScratch, a.scratch_val + (gw * 2 + 1) * kScratch};
-        uint16_t* smeta[2] = {a.scratch_meta + (gw * 2 + 0) * kScratch, a.scratch_meta + (gw * 2 + 1) * kScratch};
-        int* base_s = ebase[e];             // [4][32] reserved positions of the pending item
         uint32_t ic = 0;
         int64_t item = blockIdx.x;
         Item it{};
@@ -234,26 +225,6 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                 nextc.q = -1;
                 nextc.pair = -1;
             }
-        };
-        // pending (previous) item: entries staged in list pb, per-lane bases of its 4 chunks
-        int pend_n = 0, pb = 0, pcolbuf = 0;
-        int pbase[4] = {0, 0, 0, 0};
-        auto commit_pending = [&]() {
-            if (pend_n == 0) return;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) base_s[c * 32 + lane] = pbase[c];
-            __syncwarp();
-            const ColC* pcb = colc + pcolbuf * kTN;
-            for (int x = lane; x < pend_n; x += 32) {
-                const uint64_t val = sval[pb][x];
-                const uint32_t m = smeta[pb][x];
-                const int c = m >> 10, i = (m >> 5) & 31, off = m & 31;
-                const int pos = base_s[c * 32 + i] + off;
-                const int q = pcb[half * (kTN / 2) + c * 32 + i].q;
-                if (pos < a.cap) a.buf[(size_t)q * a.cap + pos] = val;
-            }
-            __syncwarp();
-            pend_n = 0;
         };
         if (item < total) {
             it = decode_item(a, item);
@@ -279,23 +250,23 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
             const int pc = vok ? (int)a.pcnt[slot] : 0;
             const float g1 = (kLB && vok) ? a.g1[slot] : 0.f;
             const uint32_t row = vok ? a.rows[slot] : 0u;
-            const int lb = ic & 1;  // staging list of this item
-            int n = 0;              // staged entries (warp-uniform)
-            int mycnt[4] = {0, 0, 0, 0};
             tc::mbar_wait(&accf_bar[b], ub & 1);
             tc::fence_after_sync();
-#pragma unroll
-            for (int h = 0; h < kTN / 64; ++h) {
+#pragma unroll 1
+            for (int h = 0; h < ((a.experiment & 1) ? 0 : kTN / 64); ++h) {
                 const int col0 = half * (kTN / 2) + h * 32;
                 if (col0 >= it.ncols) break;  // warp-uniform
                 uint32_t acc[32];
                 tc::tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * kTN + col0), acc);
+                // phase 1: keys + survivor ballots of 32 columns; lane i keeps column i's ballot
+                float key[32];
+                uint32_t myballot = 0u;
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
                     const ColC& cc = cb[col0 + i];  // empty columns have tau = -inf
                     const int ip = (int)acc[i];
                     const float est = rabitq_est(ip, pc, fac, cc.c);
-                    const float key = rank_key<kLB>(est, cc.epsnq, g1);
+                    key[i] = rank_key<kLB>(est, cc.epsnq, g1);
                     if constexpr (kDump) {
                         if (vok && col0 + i < it.ncols) {
                             const int64_t di = (a.item_off[cc.pair] + (v >> 5)) * 32 + (v & 31);
@@ -307,42 +278,40 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                     }
                     bool sv;
                     if constexpr (kRetry) {  // exact (key, row) <= tau64 (overflow re-scan)
-                        const uint32_t ko = f2o(key), to = f2o(cc.tau);
+                        const uint32_t ko = f2o(key[i]), to = f2o(cc.tau);
                         sv = vok && (ko < to || (ko == to && row <= (uint32_t)cc.pair));
                     } else {
-                        sv = vok && key <= cc.tau;
+                        sv = vok && key[i] <= cc.tau;
                     }
                     const uint32_t bal = __ballot_sync(0xFFFFFFFFu, sv);
-                    if (bal) {  // warp-uniform
-                        const int off = __popc(bal & ((1u << lane) - 1u));
-                        if (sv) {
-                            sval[lb][n + off] = make_key(key, row);
-                            smeta[lb][n + off] = (uint16_t)((h << 10) | (i << 5) | off);
+                    if (lane == i) myballot = bal;
+                }
+                // phase 2: one atomic per surviving column, all issued together by their lanes
+                const uint32_t cols = __ballot_sync(0xFFFFFFFFu, myballot != 0u);
+                if (cols) {
+                    int mybase = 0;
+                    if (myballot) mybase = atomicAdd(&a.cnt[cb[col0 + lane].q], __popc(myballot));
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        if (!(cols >> i & 1u)) continue;  // warp-uniform
+                        const uint32_t bal = __shfl_sync(0xFFFFFFFFu, myballot, i);
+                        const int base = __shfl_sync(0xFFFFFFFFu, mybase, i);
+                        if (bal >> lane & 1u) {
+                            const int pos = base + __popc(bal & ((1u << lane) - 1u));
+                            if (pos < a.cap) a.buf[(size_t)cb[col0 + i].q * a.cap + pos] = make_key(key[i], row);
                         }
-                        if (lane == i) mycnt[h] = __popc(bal);
-                        n += __popc(bal);
                     }
                 }
             }
             tc::fence_before_sync();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&acce_bar[b]);  // accumulator b may be overwritten
-            // finish the previous item (its atomics have long returned), then reserve this one's
-            commit_pending();
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-                pbase[c] = mycnt[c] ? atomicAdd(&a.cnt[cb[half * (kTN / 2) + c * 32 + lane].q], mycnt[c]) : 0;
-            pend_n = n;
-            pb = lb;
-            pcolbuf = b;
             // publish the next item's column constants into the other buffer (its last
-            // readers -- item ic - 1 and its commit above -- are done)
-            tc::named_barrier(1, kEpiWarps * 32);
+            // readers finished item ic - 1 before the previous barrier)
             if (nitem < total) colc[(b ^ 1) * kTN + et] = nextc;
             tc::named_barrier(1, kEpiWarps * 32);
             it = nit;
         }
-        commit_pending();
     }
     tc::fence_before_sync();
     __syncthreads();
@@ -511,18 +480,6 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
         a.gpair, a.npairs, a.nprobe, a.D, a.qscal, a.tau, retry ? a.tau64 : nullptr, a.eps0, gcolc.p);
     RQ_CHECK_LAUNCH();
     a.gcolc = gcolc.p;
-    WBuf<uint64_t> sval;
-    WBuf<uint16_t> smeta;
-    {
-        int d = 0, n = 148;
-        RQ_CUDA(cudaGetDevice(&d));
-        RQ_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d));
-        const size_t entries = (size_t)n * kEpiWarps * 2 * kScratch;
-        sval.alloc(entries, st);
-        smeta.alloc(entries, st);
-    }
-    a.scratch_val = sval.p;
-    a.scratch_meta = smeta.p;
     int dev = 0, sms = 148;
     RQ_CUDA(cudaGetDevice(&dev));
     RQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));

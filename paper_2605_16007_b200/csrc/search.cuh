@@ -46,8 +46,7 @@ struct ScanArgs {
     const int64_t* list_items; // [nlist + 1] prefix of (128-vector tile, 128-query group) items
     const uint16_t* pcnt;      // [nslots] popcount of each code
     const ColC* gcolc;         // [npairs] column constants in grouped order
-    uint64_t* scratch_val;     // grouped scan: per-warp survivor staging lists
-    uint16_t* scratch_meta;
+    int experiment;            // diagnostics (RABITQ_IMMA_EXPERIMENT): 1 skip epilogue math, 2 skip UMMAs
 };
 
 template <typename T>
