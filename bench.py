@@ -104,9 +104,11 @@ def workload(args):
 
 
 def build_shard(s, rank, world, dev, rq):
+    from paper_2605_16007_b200 import dist as rdist
+
     """Generate this rank's contiguous id slice on the device and build its
     shard (rank 0 trains P and the centroids, the others reuse them)."""
-    lo, hi = synth.shard_range(s.N, rank, world)
+    lo, hi = rdist.shard_range(s.N, rank, world)
     cen = synth.centres(s, dev)
     t0 = time.time()
     X = synth.base_rows(s, lo, hi, dev, cen=cen)
@@ -126,8 +128,7 @@ def build_shard(s, rank, world, dev, rq):
             ex = idx.export()
             P.copy_(torch.from_numpy(ex["rotation"]))
             C.copy_(torch.from_numpy(ex["centroids"]))
-        torch.distributed.broadcast(P, 0)
-        torch.distributed.broadcast(C, 0)
+        rdist.broadcast_params(P, C)
         if rank != 0:
             idx = rq.Index(X, nlist=s.nlist, seed=s.build_seed, borrow=True, id_offset=lo, rotation=P,
                            centroids_rot=C)
@@ -142,6 +143,7 @@ def l2_flush(buf):
 
 def run_ours(args):
     import paper_2605_16007_b200 as rq
+    from paper_2605_16007_b200 import dist as rdist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -154,9 +156,8 @@ def run_ours(args):
     idx, X, Q = build_shard(s, rank, world, dev, rq)
     comm = None
     if world > 1:
-        uid = [rq.Comm.unique_id() if rank == 0 else None]
-        torch.distributed.broadcast_object_list(uid, 0)
-        comm = rq.Comm(uid[0], rank, world, local)
+        uid = rdist.share_unique_id(rq.Comm.unique_id() if rank == 0 else None)
+        comm = rq.Comm(uid, rank, world, local)
     stream = torch.cuda.Stream(dev)  # the library's kernels and the timing events share this stream
     ids = torch.empty(s.nq, s.k, dtype=torch.int64, device=dev)
     dist = torch.empty(s.nq, s.k, dtype=torch.float32, device=dev)
@@ -293,7 +294,8 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": round(qps, 1), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "u32 codes x 4-bit query planes (popc) / f32",
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": ("u8 (tcgen05 kind::i8: 0/1 codes x 4-bit query) + f32 estimator/re-rank" if imma
+                  else "u32 bit-planes (AND+POPC) + f32 estimator/re-rank"),
         "data": "synthetic (synth/ seeded Gaussian mixture, generated on device)",
         "config": {"workload": f"CFG{s.cfg}", "D": s.D, "N": s.N, "nlist": s.nlist, "nq": s.nq, "nprobe": s.nprobe,
                    "k": s.k, "n_rerank": s.M, "kind": s.kind, "parallelism": f"list-shards x{world}",
