@@ -9,6 +9,7 @@
 #include <memory>
 #include <new>
 #include <string>
+#include <cstdlib>
 #include <vector>
 
 #include "index.cuh"
@@ -240,6 +241,10 @@ static void search_local(const rabitq_index* idx, const float* Q, int64_t nq, in
     cfg.seed_max = o.seed_max > 0 ? o.seed_max : std::min(32768, std::max(4096, 4 * M));
     cfg.seed_max = std::max(cfg.seed_max, M);
     RQ_REQUIRE(cfg.seed_max <= 49152, RABITQ_ERR_INVALID_ARGUMENT, "seed_max too large");
+    {
+        const char* rr = getenv("RABITQ_REFINE_RANK");  // diagnostics override
+        cfg.refine_rank = rr ? atoi(rr) : std::min(4, std::max(1, nprobe / 16));
+    }
 
     const int D = idx->D, W = idx->W;
     // batch so that per-batch workspace stays bounded (~3 GiB)

@@ -351,11 +351,14 @@ __global__ void gather_rows_kernel(const int32_t* __restrict__ sub, int64_t n, c
     }
 }
 
-// pairs of the flagged (overflowed) queries
-__global__ void compact_flagged_kernel(const int* __restrict__ flags, int64_t npairs, int nprobe,
+// pairs of the flagged (overflowed) queries, or (flags == nullptr) the pairs of
+// probe rank < max_rank (each query's nearest lists)
+__global__ void compact_flagged_kernel(const int* __restrict__ flags, int max_rank, int64_t npairs, int nprobe,
                                        int32_t* __restrict__ sub, int* __restrict__ n) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npairs; p += (int64_t)gridDim.x * blockDim.x)
-        if (flags[p / nprobe]) sub[atomicAdd(n, 1)] = (int32_t)p;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npairs; p += (int64_t)gridDim.x * blockDim.x) {
+        const bool take = flags ? flags[p / nprobe] != 0 : (p % nprobe) < max_rank;
+        if (take) sub[atomicAdd(n, 1)] = (int32_t)p;
+    }
 }
 
 // column constants of every grouped row (one 32-byte record per (query, list) pair)
@@ -438,14 +441,14 @@ void prepare_groups(const rabitq_index* idx, const int32_t* probes, int64_t n, c
 }
 
 int64_t regroup_flagged(const rabitq_index* idx, const int32_t* probes, int64_t npairs, int nprobe, const int* flags,
-                        const Groups& full, Groups& sub, cudaStream_t st, int& launches) {
+                        int max_rank, const Groups& full, Groups& sub, cudaStream_t st, int& launches) {
     WBuf<int32_t> list;
     list.alloc((size_t)npairs, st);
     WBuf<int> cnt;
     cnt.alloc(1, st);
     RQ_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int), st));
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((npairs + 255) / 256, 2048));
-    compact_flagged_kernel<<<grid, 256, 0, st>>>(flags, npairs, nprobe, list.p, cnt.p);
+    compact_flagged_kernel<<<grid, 256, 0, st>>>(flags, max_rank, npairs, nprobe, list.p, cnt.p);
     RQ_CHECK_LAUNCH();
     int n = 0;
     RQ_CUDA(cudaMemcpyAsync(&n, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, st));

@@ -73,7 +73,7 @@ struct Groups {
 void prepare_groups(const rabitq_index* idx, const int32_t* probes, int64_t n, const int32_t* sub, Groups& g,
                     cudaStream_t st, int& launches);
 int64_t regroup_flagged(const rabitq_index* idx, const int32_t* probes, int64_t npairs, int nprobe, const int* flags,
-                        const Groups& full, Groups& sub, cudaStream_t st, int& launches);
+                        int max_rank, const Groups& full, Groups& sub, cudaStream_t st, int& launches);
 bool imma_wanted(const rabitq_index* idx, int64_t npairs, int scan_path);
 
 struct RerankArgs {
@@ -105,6 +105,7 @@ struct SearchCfg {
     float eps0 = 1.9f;
     int cap = 0;
     int seed_max = 0;
+    int refine_rank = 0;  // > 0: refine tau with a tensor-core pass over each query's nearest lists
 };
 
 struct DebugOut {  // device-or-host pointers (cudaMemcpyDefault), all nullable
