@@ -282,12 +282,15 @@ def run_ours(args):
     # ---- recall@k vs exact on a query sample (torch brute force, outside the timed region) ----
     rec = None
     if world == 1 and args.recall:
-        nsub = min(100, s.nq)
+        nsub = min(100 if s.N <= 10_000_000 else 20, s.nq)
+        step = max(1, (1 << 28) // (s.D * 4 * 8))  # rows per chunk (~1 GiB of fp32 temporaries)
         gt = []
-        for q0 in range(0, nsub, 25):
-            dd = torch.cdist(Q[q0:q0 + 25].double(), X.double())
+        for q in range(nsub):
+            dd = torch.empty(s.N, dtype=torch.float64, device=dev)
+            for r0 in range(0, s.N, step):
+                dd[r0:r0 + step] = (X[r0:r0 + step] - Q[q]).pow(2).sum(1, dtype=torch.float64)
             gt.append(torch.topk(dd, s.k, largest=False).indices.cpu())
-        gt = torch.cat(gt).numpy()
+        gt = torch.stack(gt).numpy()
         got = ids[:nsub].cpu().numpy()
         rec = float(np.mean([len(set(a_.tolist()) & set(b_.tolist())) / s.k for a_, b_ in zip(got, gt)]))
 
