@@ -12,13 +12,14 @@
 // S back with tcgen05.ld and applies the same estimator + threshold as the
 // popc scan (rabitq_est), so both paths produce bit-identical keys.
 //
-// Work item = (list, 128-vector tile, group of <= 256 queries); one
-// persistent CTA per SM strides over the items.  The K loop runs in 128-byte
-// chunks through a 4-stage shared-memory ring: TMA brings the query rows (B,
-// 128-byte swizzle), producer warps expand the code bits (A); a single thread
-// issues the UMMAs into one of two TMEM accumulators (2 x 256 columns) while
-// 8 epilogue warps drain the other (warp-specialised, mbarrier-pipelined).
-// UMMA N is the group size rounded up to 16, so empty columns cost nothing.
+// Work item = (list, group of <= NG queries, range of <= 8 vector tiles); one
+// persistent CTA per SM strides over the items.  The group's int8 query rows
+// (B, every K chunk, 128-byte swizzle) are loaded ONCE per item by TMA and stay
+// resident in shared memory (NG = 256 for D <= 512, 128 at D = 960); producer
+// warps expand each 128-vector code tile (A) chunk by chunk into a 4-stage
+// ring; a single thread issues the UMMAs into one of two TMEM accumulators
+// (2 x 256 columns) while 8 epilogue warps drain the other.  UMMA N is the
+// group size rounded up to 16, so empty columns cost nothing.
 //
 // This ignores query boundaries for scheduling and re-opens the
 // list grouping the paper rejected for its NPU pipeline: on B200 it
@@ -38,24 +39,31 @@ namespace rabitq {
 namespace {
 
 constexpr int kTM = 128;                   // vectors per tile (UMMA M)
-constexpr int kTN = 256;                   // queries per group (max UMMA N)
-constexpr int kKC = 128;                   // bytes of K per stage (one 128-byte swizzle row of B)
-constexpr int kStages = 4;
+constexpr int kTN = 256;                   // max queries per group (max UMMA N); grouped-row padding
+constexpr int kKC = 128;                   // bytes of K per chunk (one 128-byte swizzle row of B)
+constexpr int kStages = 4;                 // A (expanded code) ring
 constexpr int kStageA = kTM * kKC;         // 16 KB, canonical no-swizzle K-major
-constexpr int kStageB = kTN * kKC;         // 32 KB, TMA 128-byte swizzle
+constexpr int kBRes = 128 * 1024;          // resident query operand (all K chunks of one group)
 constexpr int kSBO = (kKC / 16) * 128;     // A: distance between 8-row core-matrix groups
 constexpr int kBoxRows = 32;               // TMA box = 32 query rows x 128 bytes
+constexpr int kTilesPerItem = 8;           // vector tiles per work item (B loaded once per item)
 constexpr int kProdWarps = 4, kEpiWarps = 8;
 constexpr int kMmaWarp = kProdWarps;       // warp 4 issues the UMMAs (and owns TMEM)
 constexpr int kEpiWarp0 = kProdWarps + 1;  // warps 5..12
 constexpr int kNT = (kProdWarps + 1 + kEpiWarps) * 32;  // 416 threads
 constexpr int kTmemCols = 2 * kTN;         // double-buffered accumulator: 512 columns
 
+// queries per group so that all K chunks of a group fit the resident B region
+__host__ __device__ inline int group_cols(int Dp) {
+    const int nch = (Dp + kKC - 1) / kKC;
+    int n = (kBRes / (nch * kKC)) / kBoxRows * kBoxRows;
+    return n > kTN ? kTN : n;
+}
 
 struct Item {
     int j;
-    int64_t L, tv, slot0, grow0;
-    int ncols, ncols16, nboxes;
+    int64_t L, t0, slot_base, grow0;
+    int ntiles, ncols, ncols16, nboxes;
 };
 
 // 16 code bits -> 16 bytes of 0/1 (x * 0x00204081 spreads 4 bits to 4 bytes)
@@ -68,7 +76,8 @@ __device__ __forceinline__ uint4 expand16(uint32_t b) {
     return r;
 }
 
-__device__ __forceinline__ Item decode_item(const ScanArgs& a, int64_t item) {
+// item = (list, group of <= NG queries, range of <= kTilesPerItem vector tiles)
+__device__ __forceinline__ Item decode_item(const ScanArgs& a, int NG, int64_t item) {
     int64_t lo = 0, hi = a.nlist;
     while (hi - lo > 1) {
         const int64_t mid = (lo + hi) >> 1;
@@ -80,47 +89,55 @@ __device__ __forceinline__ Item decode_item(const ScanArgs& a, int64_t item) {
     it.L = __ldg(a.list_off + lo + 1) - __ldg(a.list_off + lo);
     const int64_t gs = __ldg(a.gstart + lo);
     const int64_t G = __ldg(a.gstart + lo + 1) - gs;
-    const int64_t ng = (G + kTN - 1) / kTN;
+    const int64_t ntl = (it.L + kTM - 1) / kTM;
+    const int64_t nti = (ntl + kTilesPerItem - 1) / kTilesPerItem;
     const int64_t local = item - __ldg(a.list_items + lo);
-    it.tv = local / ng;
-    const int64_t g = local % ng;
-    it.slot0 = __ldg(a.slot_off + lo) + it.tv * kTM;
-    it.grow0 = gs + g * kTN;
-    const int64_t rem = G - g * kTN;
-    it.ncols = (int)(rem < kTN ? rem : kTN);
+    const int64_t g = local / nti, ti = local % nti;
+    it.t0 = ti * kTilesPerItem;
+    const int64_t nt = ntl - it.t0;
+    it.ntiles = (int)(nt < kTilesPerItem ? nt : kTilesPerItem);
+    it.slot_base = __ldg(a.slot_off + lo);
+    it.grow0 = gs + g * NG;
+    const int64_t rem = G - g * NG;
+    it.ncols = (int)(rem < NG ? rem : NG);
     it.ncols16 = (it.ncols + 15) & ~15;
     it.nboxes = (it.ncols + kBoxRows - 1) / kBoxRows;
     return it;
 }
 
 // Warp-specialised persistent kernel, one CTA per SM:
-//   warps 0-3  producers: TMA of the query rows (B) + bit -> byte expansion of
-//              the code tile (A) into a 4-stage shared-memory ring
-//   warp 4     MMA issuer: 4 UMMA (K = 32 each) per stage into one of two
-//              TMEM accumulators; tcgen05.commit frees stages / publishes tiles
+//   warps 0-3  producers: one TMA load of the group's query rows (B, all K,
+//              resident for the whole item) + bit -> byte expansion of each
+//              code tile (A) into a 4-stage shared-memory ring
+//   warp 4     MMA issuer: 4 UMMA (K = 32 each) per 128-byte chunk into one of
+//              two TMEM accumulators per vector tile; tcgen05.commit frees A
+//              stages, publishes accumulators and frees B after the item
 //   warps 5-12 epilogue: tcgen05.ld the int32 inner products, fused
 //              estimator (+ bound), threshold, survivor append
 template <bool kLB, bool kDump, bool kRetry>
 __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant__ CUtensorMap tmapB, ScanArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-    uint8_t* stA = smem;                                   // [kStages][kStageA]
-    uint8_t* stB = smem + kStages * kStageA;               // [kStages][kStageB]
+    uint8_t* Bres = smem;                    // [nchunks][NG rows][128 B], 128-byte swizzle
+    uint8_t* stA = smem + kBRes;             // [kStages][kStageA]
     __shared__ __align__(16) ColC colc[2 * kTN];
-    __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], accf_bar[2], acce_bar[2];
+    __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], accf_bar[2], acce_bar[2], bfull_bar,
+        bfree_bar;
     __shared__ uint32_t tmem_base_s;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (warp == kMmaWarp) tc::tmem_alloc(&tmem_base_s, kTmemCols);
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
-            tc::mbar_init(&full_bar[s], kProdWarps * 32 + 1);
+            tc::mbar_init(&full_bar[s], kProdWarps * 32);
             tc::mbar_init(&empty_bar[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             tc::mbar_init(&accf_bar[b], 1);
             tc::mbar_init(&acce_bar[b], kEpiWarps);
         }
+        tc::mbar_init(&bfull_bar, 1);
+        tc::mbar_init(&bfree_bar, 1);
         tc::prefetch_tmap(&tmapB);
     }
     tc::fence_before_sync();
@@ -130,88 +147,101 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
 
     const int64_t total = a.list_items[a.nlist];
     const int nchunks = (a.Dp + kKC - 1) / kKC;
+    const int NG = group_cols(a.Dp);
+    const int bchunk = NG * kKC;             // bytes of one K chunk of the resident B
 
     if (warp < kProdWarps) {
         // ================= producers =================
         const int r = tid;  // tile row 0..127 = vector
-        uint32_t gc = 0;    // global chunk counter (stage ring position)
-        for (int64_t item = blockIdx.x; item < total; item += gridDim.x) {
-            const Item it = decode_item(a, item);
-            const int64_t slot = it.slot0 + r;
-            const uint32_t* cbase = a.codes + ((size_t)(slot >> 5) * a.W) * 32 + (slot & 31);
-            uint32_t wnext[4];
-#pragma unroll
-            for (int t = 0; t < 4; ++t) wnext[t] = (t * 32 < min(kKC, a.Dp)) ? __ldg(cbase + (size_t)t * 32) : 0u;
-            for (int c = 0; c < nchunks; ++c, ++gc) {
-                const int s = gc % kStages;
-                const uint32_t u = gc / kStages;
-                const int kbytes = min(kKC, a.Dp - c * kKC);
-                uint32_t wcur[4];
-#pragma unroll
-                for (int t = 0; t < 4; ++t) wcur[t] = wnext[t];
-                if (c + 1 < nchunks) {  // prefetch the next chunk's code words
-                    const int kb2 = min(kKC, a.Dp - (c + 1) * kKC);
-#pragma unroll
-                    for (int t = 0; t < 4; ++t)
-                        wnext[t] = (t * 32 < kb2) ? __ldg(cbase + (size_t)((c + 1) * 4 + t) * 32) : 0u;
-                }
-                if (u > 0) tc::mbar_wait(&empty_bar[s], (u - 1) & 1);
-                if (tid == 0) {
-                    tc::mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(it.nboxes * kBoxRows * kKC));
+        uint32_t gc = 0, ic = 0;
+        for (int64_t item = blockIdx.x; item < total; item += gridDim.x, ++ic) {
+            const Item it = decode_item(a, NG, item);
+            if (tid == 0) {
+                if (ic > 0) tc::mbar_wait(&bfree_bar, (ic - 1) & 1);  // previous item's UMMAs retired
+                tc::mbar_arrive_expect_tx(&bfull_bar, (uint32_t)(it.nboxes * nchunks * kBoxRows * kKC));
+                for (int c = 0; c < nchunks; ++c)
                     for (int bx = 0; bx < it.nboxes; ++bx)
-                        tc::tma_load_2d(stB + s * kStageB + bx * kBoxRows * kKC, &tmapB, &full_bar[s], c * kKC,
+                        tc::tma_load_2d(Bres + c * bchunk + bx * kBoxRows * kKC, &tmapB, &bfull_bar, c * kKC,
                                         (int)(it.grow0 + bx * kBoxRows));
-                }
-                uint8_t* A = stA + s * kStageA + (r >> 3) * kSBO + (r & 7) * 16;
+            }
+            for (int t = 0; t < it.ntiles; ++t) {
+                const int64_t slot = it.slot_base + (it.t0 + t) * kTM + r;
+                const uint32_t* cbase = a.codes + ((size_t)(slot >> 5) * a.W) * 32 + (slot & 31);
+                uint32_t wnext[4];
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    if (t * 32 >= kbytes) break;
-                    *reinterpret_cast<uint4*>(A + (2 * t) * 128) = expand16(wcur[t] & 0xFFFFu);
-                    *reinterpret_cast<uint4*>(A + (2 * t + 1) * 128) = expand16(wcur[t] >> 16);
+                for (int q = 0; q < 4; ++q) wnext[q] = (q * 32 < min(kKC, a.Dp)) ? __ldg(cbase + (size_t)q * 32) : 0u;
+                for (int c = 0; c < nchunks; ++c, ++gc) {
+                    const int s = gc % kStages;
+                    const uint32_t u = gc / kStages;
+                    const int kbytes = min(kKC, a.Dp - c * kKC);
+                    uint32_t wcur[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) wcur[q] = wnext[q];
+                    if (c + 1 < nchunks) {  // prefetch the next chunk's code words
+                        const int kb2 = min(kKC, a.Dp - (c + 1) * kKC);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            wnext[q] = (q * 32 < kb2) ? __ldg(cbase + (size_t)((c + 1) * 4 + q) * 32) : 0u;
+                    }
+                    if (u > 0) tc::mbar_wait(&empty_bar[s], (u - 1) & 1);
+                    uint8_t* A = stA + s * kStageA + (r >> 3) * kSBO + (r & 7) * 16;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        if (q * 32 >= kbytes) break;
+                        *reinterpret_cast<uint4*>(A + (2 * q) * 128) = expand16(wcur[q] & 0xFFFFu);
+                        *reinterpret_cast<uint4*>(A + (2 * q + 1) * 128) = expand16(wcur[q] >> 16);
+                    }
+                    tc::fence_proxy_async();
+                    tc::mbar_arrive(&full_bar[s]);
                 }
-                tc::fence_proxy_async();
-                tc::mbar_arrive(&full_bar[s]);
             }
         }
     } else if (warp == kMmaWarp) {
         // ================= MMA issuer =================
-        uint32_t gc = 0, ic = 0;
+        uint32_t gc = 0, tcnt = 0, ic = 0;
         for (int64_t item = blockIdx.x; item < total; item += gridDim.x, ++ic) {
-            const Item it = decode_item(a, item);
+            const Item it = decode_item(a, NG, item);
             const uint32_t idesc = tc::idesc_i8(kTM, it.ncols16);
-            const int b = ic & 1;
-            const uint32_t ub = ic >> 1;
-            if (ub > 0) tc::mbar_wait(&acce_bar[b], (ub - 1) & 1);
+            tc::mbar_wait(&bfull_bar, ic & 1);
             tc::fence_after_sync();
-            const uint32_t dacc = tmem + (uint32_t)(b * kTN);
-            for (int c = 0; c < nchunks; ++c, ++gc) {
-                const int s = gc % kStages;
-                const uint32_t u = gc / kStages;
-                const int kbytes = min(kKC, a.Dp - c * kKC);
-                tc::mbar_wait(&full_bar[s], u & 1);
+            const uint32_t baddr = tc::smem_u32(Bres);
+            for (int t = 0; t < it.ntiles; ++t, ++tcnt) {
+                const int b = tcnt & 1;
+                const uint32_t ub = tcnt >> 1;
+                if (ub > 0) tc::mbar_wait(&acce_bar[b], (ub - 1) & 1);
                 tc::fence_after_sync();
-                if (lane == 0) {
-                    const uint32_t aaddr = tc::smem_u32(stA + s * kStageA), baddr = tc::smem_u32(stB + s * kStageB);
-                    const int nks = (a.experiment & 2) ? ((c == 0) ? 1 : 0) : kbytes / 32;
-                    for (int ks = 0; ks < nks; ++ks) {
-                        const uint64_t ad = tc::smem_desc(aaddr + ks * 256, 128, kSBO);
-                        const uint64_t bd = tc::smem_desc_sw128(baddr + ks * 32);
-                        tc::mma_i8(dacc, ad, bd, idesc, (c > 0 || ks > 0) ? 1u : 0u);
+                const uint32_t dacc = tmem + (uint32_t)(b * kTN);
+                for (int c = 0; c < nchunks; ++c, ++gc) {
+                    const int s = gc % kStages;
+                    const uint32_t u = gc / kStages;
+                    const int kbytes = min(kKC, a.Dp - c * kKC);
+                    tc::mbar_wait(&full_bar[s], u & 1);
+                    tc::fence_after_sync();
+                    if (lane == 0) {
+                        const uint32_t aaddr = tc::smem_u32(stA + s * kStageA);
+                        const int nks = (a.experiment & 2) ? ((c == 0) ? 1 : 0) : kbytes / 32;
+                        for (int ks = 0; ks < nks; ++ks) {
+                            const uint64_t ad = tc::smem_desc(aaddr + ks * 256, 128, kSBO);
+                            const uint64_t bd = tc::smem_desc_sw128(baddr + c * bchunk + ks * 32);
+                            tc::mma_i8(dacc, ad, bd, idesc, (c > 0 || ks > 0) ? 1u : 0u);
+                        }
+                        tc::commit(&empty_bar[s]);                       // A stage s free once these retire
+                        if (c == nchunks - 1) tc::commit(&accf_bar[b]);  // accumulator b complete
                     }
-                    tc::commit(&empty_bar[s]);                       // stage s free once these UMMAs retire
-                    if (c == nchunks - 1) tc::commit(&accf_bar[b]);  // accumulator b complete
+                    __syncwarp();
                 }
-                __syncwarp();
             }
+            if (lane == 0) tc::commit(&bfree_bar);  // resident B free once the item's UMMAs retire
+            __syncwarp();
         }
     } else {
         // ================= epilogue =================
         const int e = warp - kEpiWarp0;     // 0..7
         const int quarter = warp & 3;       // TMEM lanes this warp may access: 32 * (warp % 4) ..
-        const int half = e >> 2;            // column half
+        const int half = e >> 2;            // interleaved 32-column chunks: half, half + 2, ...
         const int r = quarter * 32 + lane;  // tile row = vector
         const int et = e * 32 + lane;       // 0..255 among epilogue threads
-        uint32_t ic = 0;
+        uint32_t ic = 0, tcnt = 0;
         int64_t item = blockIdx.x;
         Item it{};
         ColC nextc;
@@ -227,88 +257,90 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
             }
         };
         if (item < total) {
-            it = decode_item(a, item);
+            it = decode_item(a, NG, item);
             fetch_colc(it);
             colc[et] = nextc;
         }
         tc::named_barrier(1, kEpiWarps * 32);
         for (; item < total; item += gridDim.x, ++ic) {
-            const int b = ic & 1;
-            const uint32_t ub = ic >> 1;
-            const ColC* cb = colc + b * kTN;
+            const int cbuf = ic & 1;
+            const ColC* cb = colc + cbuf * kTN;
             // prefetch the next item's column constants (latency hidden by this item)
             const int64_t nitem = item + gridDim.x;
             Item nit{};
             if (nitem < total) {
-                nit = decode_item(a, nitem);
+                nit = decode_item(a, NG, nitem);
                 fetch_colc(nit);
             }
-            const int64_t v = it.tv * kTM + r;
-            const bool vok = v < it.L;
-            const int64_t slot = it.slot0 + r;
-            const float2 fac = vok ? a.fac[slot] : make_float2(0.f, 0.f);
-            const int pc = vok ? (int)a.pcnt[slot] : 0;
-            const float g1 = (kLB && vok) ? a.g1[slot] : 0.f;
-            const uint32_t row = vok ? a.rows[slot] : 0u;
-            tc::mbar_wait(&accf_bar[b], ub & 1);
-            tc::fence_after_sync();
+            for (int t = 0; t < it.ntiles; ++t, ++tcnt) {
+                const int b = tcnt & 1;
+                const uint32_t ub = tcnt >> 1;
+                const int64_t v = (it.t0 + t) * kTM + r;
+                const bool vok = v < it.L;
+                const int64_t slot = it.slot_base + v;
+                const float2 fac = vok ? a.fac[slot] : make_float2(0.f, 0.f);
+                const int pc = vok ? (int)a.pcnt[slot] : 0;
+                const float g1 = (kLB && vok) ? a.g1[slot] : 0.f;
+                const uint32_t row = vok ? a.rows[slot] : 0u;
+                tc::mbar_wait(&accf_bar[b], ub & 1);
+                tc::fence_after_sync();
 #pragma unroll 1
-            for (int h = 0; h < ((a.experiment & 1) ? 0 : kTN / 64); ++h) {
-                const int col0 = half * (kTN / 2) + h * 32;
-                if (col0 >= it.ncols) break;  // warp-uniform
-                uint32_t acc[32];
-                tc::tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * kTN + col0), acc);
-                // phase 1: keys + survivor ballots of 32 columns; lane i keeps column i's ballot
-                float key[32];
-                uint32_t myballot = 0u;
+                for (int hc = half; hc * 32 < ((a.experiment & 1) ? 0 : it.ncols); hc += 2) {
+                    const int col0 = hc * 32;
+                    uint32_t acc[32];
+                    tc::tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * kTN + col0), acc);
+                    // phase 1: keys + survivor ballots of 32 columns; lane i keeps column i's ballot
+                    float key[32];
+                    uint32_t myballot = 0u;
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const ColC& cc = cb[col0 + i];  // empty columns have tau = -inf
-                    const int ip = (int)acc[i];
-                    const float est = rabitq_est(ip, pc, fac, cc.c);
-                    key[i] = rank_key<kLB>(est, cc.epsnq, g1);
-                    if constexpr (kDump) {
-                        if (vok && col0 + i < it.ncols) {
-                            const int64_t di = (a.item_off[cc.pair] + (v >> 5)) * 32 + (v & 31);
-                            if (di < a.dump_cap) {
-                                a.dump_ip[di] = ip;
-                                a.dump_est[di] = est;
+                    for (int i = 0; i < 32; ++i) {
+                        const ColC& cc = cb[col0 + i];  // empty columns have tau = -inf
+                        const int ip = (int)acc[i];
+                        const float est = rabitq_est(ip, pc, fac, cc.c);
+                        key[i] = rank_key<kLB>(est, cc.epsnq, g1);
+                        if constexpr (kDump) {
+                            if (vok && col0 + i < it.ncols) {
+                                const int64_t di = (a.item_off[cc.pair] + (v >> 5)) * 32 + (v & 31);
+                                if (di < a.dump_cap) {
+                                    a.dump_ip[di] = ip;
+                                    a.dump_est[di] = est;
+                                }
+                            }
+                        }
+                        bool sv;
+                        if constexpr (kRetry) {  // exact (key, row) <= tau64 (overflow re-scan)
+                            const uint32_t ko = f2o(key[i]), to = f2o(cc.tau);
+                            sv = vok && (ko < to || (ko == to && row <= (uint32_t)cc.pair));
+                        } else {
+                            sv = vok && key[i] <= cc.tau;
+                        }
+                        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, sv);
+                        if (lane == i) myballot = bal;
+                    }
+                    // phase 2: one atomic per surviving column, all issued together by their lanes
+                    const uint32_t cols = __ballot_sync(0xFFFFFFFFu, myballot != 0u);
+                    if (cols) {
+                        int mybase = 0;
+                        if (myballot) mybase = atomicAdd(&a.cnt[cb[col0 + lane].q], __popc(myballot));
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            if (!(cols >> i & 1u)) continue;  // warp-uniform
+                            const uint32_t bal = __shfl_sync(0xFFFFFFFFu, myballot, i);
+                            const int base = __shfl_sync(0xFFFFFFFFu, mybase, i);
+                            if (bal >> lane & 1u) {
+                                const int pos = base + __popc(bal & ((1u << lane) - 1u));
+                                if (pos < a.cap) a.buf[(size_t)cb[col0 + i].q * a.cap + pos] = make_key(key[i], row);
                             }
                         }
                     }
-                    bool sv;
-                    if constexpr (kRetry) {  // exact (key, row) <= tau64 (overflow re-scan)
-                        const uint32_t ko = f2o(key[i]), to = f2o(cc.tau);
-                        sv = vok && (ko < to || (ko == to && row <= (uint32_t)cc.pair));
-                    } else {
-                        sv = vok && key[i] <= cc.tau;
-                    }
-                    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, sv);
-                    if (lane == i) myballot = bal;
                 }
-                // phase 2: one atomic per surviving column, all issued together by their lanes
-                const uint32_t cols = __ballot_sync(0xFFFFFFFFu, myballot != 0u);
-                if (cols) {
-                    int mybase = 0;
-                    if (myballot) mybase = atomicAdd(&a.cnt[cb[col0 + lane].q], __popc(myballot));
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        if (!(cols >> i & 1u)) continue;  // warp-uniform
-                        const uint32_t bal = __shfl_sync(0xFFFFFFFFu, myballot, i);
-                        const int base = __shfl_sync(0xFFFFFFFFu, mybase, i);
-                        if (bal >> lane & 1u) {
-                            const int pos = base + __popc(bal & ((1u << lane) - 1u));
-                            if (pos < a.cap) a.buf[(size_t)cb[col0 + i].q * a.cap + pos] = make_key(key[i], row);
-                        }
-                    }
-                }
+                tc::fence_before_sync();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&acce_bar[b]);  // accumulator b may be overwritten
             }
-            tc::fence_before_sync();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&acce_bar[b]);  // accumulator b may be overwritten
             // publish the next item's column constants into the other buffer (its last
             // readers finished item ic - 1 before the previous barrier)
-            if (nitem < total) colc[(b ^ 1) * kTN + et] = nextc;
+            if (nitem < total) colc[(cbuf ^ 1) * kTN + et] = nextc;
             tc::named_barrier(1, kEpiWarps * 32);
             it = nit;
         }
@@ -385,7 +417,7 @@ __global__ void colc_kernel(const int32_t* __restrict__ gpair, int64_t npairs, i
 }
 
 __global__ void list_items_kernel(int nlist, const int64_t* __restrict__ list_off, const int64_t* __restrict__ gcount,
-                                  int64_t* __restrict__ items) {
+                                  int NG, int64_t* __restrict__ items) {
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= nlist; j += gridDim.x * blockDim.x) {
         if (j == nlist) {
             items[j] = 0;
@@ -393,7 +425,8 @@ __global__ void list_items_kernel(int nlist, const int64_t* __restrict__ list_of
         }
         const int64_t L = list_off[j + 1] - list_off[j];
         const int64_t G = gcount[j];
-        items[j] = ((L + kTM - 1) / kTM) * ((G + kTN - 1) / kTN);
+        const int64_t ntl = (L + kTM - 1) / kTM;
+        items[j] = ((ntl + kTilesPerItem - 1) / kTilesPerItem) * ((G + NG - 1) / NG);
     }
 }
 
@@ -434,7 +467,8 @@ void prepare_groups(const rabitq_index* idx, const int32_t* probes, int64_t n, c
     RQ_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, g.gcount.p, g.gstart.p, nlist + 1, st));
     group_fill_kernel<<<grid, 256, 0, st>>>(probes, sub, n, g.gstart.p, g.gfill.p, g.gpos.p, g.gpair.p);
     RQ_CHECK_LAUNCH();
-    list_items_kernel<<<(nlist + 256) / 256, 256, 0, st>>>(nlist, idx->list_off, g.gcount.p, g.itemc.p);
+    list_items_kernel<<<(nlist + 256) / 256, 256, 0, st>>>(nlist, idx->list_off, g.gcount.p, group_cols(g.Dp),
+                                                           g.itemc.p);
     RQ_CHECK_LAUNCH();
     RQ_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb2, g.itemc.p, g.list_items.p, nlist + 1, st));
     launches += 7;
@@ -496,7 +530,7 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
                                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     RQ_REQUIRE(cr == CUDA_SUCCESS, RABITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
-    const size_t smem = 1024 + (size_t)kStages * (kStageA + kStageB);
+    const size_t smem = 1024 + (size_t)kBRes + (size_t)kStages * kStageA;
     const int grid = sms;
 #define RQ_IMMA(LB, DP, RT)                                                                                     \
     do {                                                                                                        \
