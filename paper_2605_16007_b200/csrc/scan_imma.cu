@@ -41,7 +41,8 @@ namespace {
 constexpr int kTM = 128;                   // vectors per tile (UMMA M)
 constexpr int kTN = 256;                   // max queries per group (max UMMA N); grouped-row padding
 constexpr int kKC = 128;                   // bytes of K per chunk (one 128-byte swizzle row of B)
-constexpr int kStages = 4;                 // A (expanded code) ring
+constexpr int kStages = 3;                 // A (expanded code) ring
+constexpr int kRawMax = 128 * 30 * 4;      // raw code tile (128 vectors x W words), W <= 30 in smem
 constexpr int kStageA = kTM * kKC;         // 16 KB, canonical no-swizzle K-major
 constexpr int kBRes = 128 * 1024;          // resident query operand (all K chunks of one group)
 constexpr int kSBO = (kKC / 16) * 128;     // A: distance between 8-row core-matrix groups
@@ -120,9 +121,10 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     uint8_t* Bres = smem;                    // [nchunks][NG rows][128 B], 128-byte swizzle
     uint8_t* stA = smem + kBRes;             // [kStages][kStageA]
+    uint32_t* raw = reinterpret_cast<uint32_t*>(stA + kStages * kStageA);  // [2][128 x W] raw code tiles
     __shared__ __align__(16) ColC colc[2 * kTN];
     __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], accf_bar[2], acce_bar[2], bfull_bar,
-        bfree_bar;
+        bfree_bar, raw_bar[2];
     __shared__ uint32_t tmem_base_s;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -138,6 +140,8 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
         }
         tc::mbar_init(&bfull_bar, 1);
         tc::mbar_init(&bfree_bar, 1);
+        tc::mbar_init(&raw_bar[0], 1);
+        tc::mbar_init(&raw_bar[1], 1);
         tc::prefetch_tmap(&tmapB);
     }
     tc::fence_before_sync();
@@ -152,10 +156,34 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
 
     if (warp < kProdWarps) {
         // ================= producers =================
+        // raw code tiles (128 x W words, contiguous) arrive by bulk copy one tile
+        // ahead into a 2-buffer ring; each thread expands its row chunk by chunk
         const int r = tid;  // tile row 0..127 = vector
-        uint32_t gc = 0, ic = 0;
-        for (int64_t item = blockIdx.x; item < total; item += gridDim.x, ++ic) {
-            const Item it = decode_item(a, NG, item);
+        const uint32_t raw_bytes = (uint32_t)(kTM * a.W * 4);
+        uint32_t gc = 0, ic = 0, rc = 0;  // chunk, item, raw-tile counters
+        int64_t item = blockIdx.x;
+        Item it{};
+        if (item < total) it = decode_item(a, NG, item);
+        // (item, tile) of the raw tile to prefetch next
+        int64_t pf_item = item;
+        Item pf_it = it;
+        int pf_t = 0;
+        auto issue_raw = [&](uint32_t k) {  // bulk copy of the next tile into raw buffer k & 1
+            if (pf_item >= total) return;
+            if (tid == 0) {
+                const int64_t slot0 = pf_it.slot_base + (pf_it.t0 + pf_t) * kTM;  // multiple of 32
+                tc::mbar_arrive_expect_tx(&raw_bar[k & 1], raw_bytes);
+                tc::bulk_load(raw + (k & 1) * (kRawMax / 4), a.codes + (size_t)(slot0 >> 5) * a.W * 32, raw_bytes,
+                              &raw_bar[k & 1]);
+            }
+            if (++pf_t >= pf_it.ntiles) {
+                pf_t = 0;
+                pf_item += gridDim.x;
+                if (pf_item < total) pf_it = decode_item(a, NG, pf_item);
+            }
+        };
+        issue_raw(0);
+        for (; item < total; item += gridDim.x, ++ic) {
             if (tid == 0) {
                 if (ic > 0) tc::mbar_wait(&bfree_bar, (ic - 1) & 1);  // previous item's UMMAs retired
                 tc::mbar_arrive_expect_tx(&bfull_bar, (uint32_t)(it.nboxes * nchunks * kBoxRows * kKC));
@@ -164,37 +192,29 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                         tc::tma_load_2d(Bres + c * bchunk + bx * kBoxRows * kKC, &tmapB, &bfull_bar, c * kKC,
                                         (int)(it.grow0 + bx * kBoxRows));
             }
-            for (int t = 0; t < it.ntiles; ++t) {
-                const int64_t slot = it.slot_base + (it.t0 + t) * kTM + r;
-                const uint32_t* cbase = a.codes + ((size_t)(slot >> 5) * a.W) * 32 + (slot & 31);
-                uint32_t wnext[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) wnext[q] = (q * 32 < min(kKC, a.Dp)) ? __ldg(cbase + (size_t)q * 32) : 0u;
+            for (int t = 0; t < it.ntiles; ++t, ++rc) {
+                issue_raw(rc + 1);  // the other buffer was released by the barrier ending tile rc - 1
+                tc::mbar_wait(&raw_bar[rc & 1], (rc >> 1) & 1);
+                const uint32_t* rt = raw + (rc & 1) * (kRawMax / 4) + (r >> 5) * a.W * 32 + (r & 31);
                 for (int c = 0; c < nchunks; ++c, ++gc) {
                     const int s = gc % kStages;
                     const uint32_t u = gc / kStages;
                     const int kbytes = min(kKC, a.Dp - c * kKC);
-                    uint32_t wcur[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) wcur[q] = wnext[q];
-                    if (c + 1 < nchunks) {  // prefetch the next chunk's code words
-                        const int kb2 = min(kKC, a.Dp - (c + 1) * kKC);
-#pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            wnext[q] = (q * 32 < kb2) ? __ldg(cbase + (size_t)((c + 1) * 4 + q) * 32) : 0u;
-                    }
                     if (u > 0) tc::mbar_wait(&empty_bar[s], (u - 1) & 1);
                     uint8_t* A = stA + s * kStageA + (r >> 3) * kSBO + (r & 7) * 16;
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         if (q * 32 >= kbytes) break;
-                        *reinterpret_cast<uint4*>(A + (2 * q) * 128) = expand16(wcur[q] & 0xFFFFu);
-                        *reinterpret_cast<uint4*>(A + (2 * q + 1) * 128) = expand16(wcur[q] >> 16);
+                        const uint32_t x = rt[(c * 4 + q) * 32];
+                        *reinterpret_cast<uint4*>(A + (2 * q) * 128) = expand16(x & 0xFFFFu);
+                        *reinterpret_cast<uint4*>(A + (2 * q + 1) * 128) = expand16(x >> 16);
                     }
                     tc::fence_proxy_async();
                     tc::mbar_arrive(&full_bar[s]);
                 }
+                tc::named_barrier(2, kProdWarps * 32);  // raw buffer rc & 1 may be refilled
             }
+            if (item + gridDim.x < total) it = decode_item(a, NG, item + gridDim.x);
         }
     } else if (warp == kMmaWarp) {
         // ================= MMA issuer =================
@@ -434,6 +454,7 @@ __global__ void list_items_kernel(int nlist, const int64_t* __restrict__ list_of
 
 bool imma_wanted(const rabitq_index* idx, int64_t npairs, int scan_path) {
     if (scan_path == RABITQ_SCAN_POPC) return false;
+    if (idx->W > kRawMax / (128 * 4)) return false;  // raw code tile must fit its smem buffer (D <= 960)
     if (scan_path == RABITQ_SCAN_IMMA) return true;
     // AUTO: the tensor-core path pays once lists are shared by enough queries
     return npairs >= (int64_t)8 * idx->nlist;
@@ -530,7 +551,7 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
                                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     RQ_REQUIRE(cr == CUDA_SUCCESS, RABITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
-    const size_t smem = 1024 + (size_t)kBRes + (size_t)kStages * kStageA;
+    const size_t smem = 1024 + (size_t)kBRes + (size_t)kStages * kStageA + 2 * (size_t)kRawMax;
     const int grid = sms;
 #define RQ_IMMA(LB, DP, RT)                                                                                     \
     do {                                                                                                        \
