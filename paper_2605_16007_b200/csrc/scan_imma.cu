@@ -131,7 +131,7 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
     if (warp == kMmaWarp) tc::tmem_alloc(&tmem_base_s, kTmemCols);
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
-            tc::mbar_init(&full_bar[s], kProdWarps * 32);
+            tc::mbar_init(&full_bar[s], 1);
             tc::mbar_init(&empty_bar[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
@@ -210,9 +210,9 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                         *reinterpret_cast<uint4*>(A + (2 * q + 1) * 128) = expand16(x >> 16);
                     }
                     tc::fence_proxy_async();
-                    tc::mbar_arrive(&full_bar[s]);
+                    tc::named_barrier(2, kProdWarps * 32);  // stage written (also releases the raw buffer after the last chunk)
+                    if (tid == 0) tc::mbar_arrive(&full_bar[s]);
                 }
-                tc::named_barrier(2, kProdWarps * 32);  // raw buffer rc & 1 may be refilled
             }
             if (item + gridDim.x < total) it = decode_item(a, NG, item + gridDim.x);
         }
