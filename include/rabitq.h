@@ -140,7 +140,9 @@ typedef struct {
     int32_t cap_per_query;   /* survivor buffer per query, 0 -> auto (max(8192, 16M)); clamped to
                                 >= 2 n_rerank; overflowing queries are re-scanned with a tighter
                                 threshold until they fit                                       */
-    int32_t seed_max;        /* vectors used to seed the pruning threshold, 0 -> auto           */
+    int32_t seed_max;        /* size of the per-query sample of probed vectors that seeds the
+                                pruning threshold, 0 -> auto (about 20 P / T, capped
+                                at 16384; P = probed vectors, T = target survivors)           */
     void* stream;            /* cudaStream_t to run on (NULL -> the index's stream); outputs
                                 in device memory are valid after that stream synchronizes     */
     rabitq_debug* debug;     /* nullable                                                       */

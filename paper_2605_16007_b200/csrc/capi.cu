@@ -238,12 +238,12 @@ static void search_local(const rabitq_index* idx, const float* Q, int64_t nq, in
     cfg.cap = o.cap_per_query > 0 ? o.cap_per_query : std::max(8192, 16 * M);
     // re-scans shrink the survivors by ~M/cap per round: keep cap >= 2M
     cfg.cap = std::max(cfg.cap, 2 * M);
-    cfg.seed_max = o.seed_max > 0 ? o.seed_max : std::min(32768, std::max(4096, 4 * M));
-    cfg.seed_max = std::max(cfg.seed_max, M);
+    // threshold-seeding sample size: 0 -> auto per query (search.cu seed_kernel)
+    cfg.seed_max = o.seed_max > 0 ? std::max(o.seed_max, M) : 0;
     RQ_REQUIRE(cfg.seed_max <= 49152, RABITQ_ERR_INVALID_ARGUMENT, "seed_max too large");
     {
-        const char* rr = getenv("RABITQ_REFINE_RANK");  // diagnostics override
-        cfg.refine_rank = rr ? atoi(rr) : std::min(4, std::max(1, nprobe / 16));
+        const char* rr = getenv("RABITQ_REFINE_RANK");  // diagnostics: tensor-core threshold refinement pass
+        cfg.refine_rank = rr ? atoi(rr) : 0;
     }
 
     const int D = idx->D, W = idx->W;

@@ -41,18 +41,22 @@ namespace {
 constexpr int kTM = 128;                   // vectors per tile (UMMA M)
 constexpr int kTN = 256;                   // max queries per group (max UMMA N); grouped-row padding
 constexpr int kKC = 128;                   // bytes of K per chunk (one 128-byte swizzle row of B)
-constexpr int kStages = 3;                 // A (expanded code) ring
-constexpr int kRawMax = 128 * 30 * 4;      // raw code tile (128 vectors x W words), W <= 30 in smem
+constexpr int kMaxChunks = 8;              // Dp <= 1024
+constexpr int kMaxStages = 10;             // A (expanded code) ring, sized from the shared-memory budget
 constexpr int kStageA = kTM * kKC;         // 16 KB, canonical no-swizzle K-major
 constexpr int kBRes = 128 * 1024;          // resident query operand (all K chunks of one group)
 constexpr int kSBO = (kKC / 16) * 128;     // A: distance between 8-row core-matrix groups
 constexpr int kBoxRows = 32;               // TMA box = 32 query rows x 128 bytes
 constexpr int kTilesPerItem = 8;           // vector tiles per work item (B loaded once per item)
-constexpr int kProdWarps = 4, kEpiWarps = 8;
-constexpr int kMmaWarp = kProdWarps;       // warp 4 issues the UMMAs (and owns TMEM)
-constexpr int kEpiWarp0 = kProdWarps + 1;  // warps 5..12
-constexpr int kNT = (kProdWarps + 1 + kEpiWarps) * 32;  // 416 threads
+constexpr int kProdWarps = 8;              // two groups of 4: group g expands words 4c+2g, 4c+2g+1 of chunk c
+constexpr int kMmaWarp = kProdWarps;       // warp 8 issues the UMMAs (and owns TMEM)
+constexpr int kLoadWarp = kProdWarps + 1;  // warp 9 streams the query operand (TMA)
+constexpr int kEpiWarp0 = kProdWarps + 2;  // warps 10..17
+constexpr int kEpiWarps = 8;
+constexpr int kNT = (kEpiWarp0 + kEpiWarps) * 32;  // 576 threads
 constexpr int kTmemCols = 2 * kTN;         // double-buffered accumulator: 512 columns
+constexpr int kWPT = 16;                   // max code words per producer thread and tile (W <= 30)
+constexpr int kSmemLimit = 227 * 1024;
 
 // queries per group so that all K chunks of a group fit the resident B region
 __host__ __device__ inline int group_cols(int Dp) {
@@ -61,21 +65,29 @@ __host__ __device__ inline int group_cols(int Dp) {
     return n > kTN ? kTN : n;
 }
 
+// shared-memory plan of one launch (host and device agree)
+struct SmemPlan {
+    int nchunks, NG, stages;
+    uint32_t off_colc, off_A, total;
+};
+__host__ __device__ inline SmemPlan smem_plan(int Dp) {
+    SmemPlan p;
+    p.nchunks = (Dp + kKC - 1) / kKC;
+    p.NG = group_cols(Dp);
+    const uint32_t bres = (uint32_t)(p.nchunks * p.NG * kKC);
+    p.off_colc = bres;                                      // [2][NG] ColC
+    p.off_A = ((p.off_colc + 2u * p.NG * (uint32_t)sizeof(ColC)) + 1023u) & ~1023u;
+    const int room = (kSmemLimit - 1024 - 2048 - (int)p.off_A) / kStageA;  // 1 KB align slack, 2 KB static
+    p.stages = room < kMaxStages ? room : kMaxStages;
+    p.total = p.off_A + (uint32_t)p.stages * kStageA + 1024u;
+    return p;
+}
+
 struct Item {
     int j;
     int64_t L, t0, slot_base, grow0;
     int ntiles, ncols, ncols16, nboxes;
 };
-
-// 16 code bits -> 16 bytes of 0/1 (x * 0x00204081 spreads 4 bits to 4 bytes)
-__device__ __forceinline__ uint4 expand16(uint32_t b) {
-    uint4 r;
-    r.x = ((b & 0xFu) * 0x00204081u) & 0x01010101u;
-    r.y = (((b >> 4) & 0xFu) * 0x00204081u) & 0x01010101u;
-    r.z = (((b >> 8) & 0xFu) * 0x00204081u) & 0x01010101u;
-    r.w = (((b >> 12) & 0xFu) * 0x00204081u) & 0x01010101u;
-    return r;
-}
 
 // item = (list, group of <= NG queries, range of <= kTilesPerItem vector tiles)
 __device__ __forceinline__ Item decode_item(const ScanArgs& a, int NG, int64_t item) {
@@ -106,31 +118,63 @@ __device__ __forceinline__ Item decode_item(const ScanArgs& a, int NG, int64_t i
     return it;
 }
 
+// 32 code bits -> 32 bytes in {0, -1} (s8), K order permuted: output byte
+// k = 4 s + t (s = 0..7, t = 0..3) holds code bit 8 t + 7 - s, the sign bit of
+// byte t of (x << s), replicated by PRMT.  The quantizer writes the query rows
+// in the same K order (kperm_dim), so the contraction is unchanged:
+//   sum_k A[k] B[k] = - sum_i b_i qbar_i = -ip.
+__device__ __forceinline__ uint32_t sgnrep(uint32_t y) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, 0, 0xBA98;" : "=r"(r) : "r"(y));
+    return r;
+}
+__device__ __forceinline__ void expand32(uint32_t x, uint4& lo, uint4& hi) {
+    lo.x = sgnrep(x);
+    lo.y = sgnrep(x * 2u);
+    lo.z = sgnrep(x * 4u);
+    lo.w = sgnrep(x * 8u);
+    hi.x = sgnrep(x * 16u);
+    hi.y = sgnrep(x * 32u);
+    hi.z = sgnrep(x * 64u);
+    hi.w = sgnrep(x * 128u);
+}
+
+// clock stamps of CTA 0 (RABITQ_SCAN_TRACE diagnostics): row idx, column slot
+#define RQ_TR(slot, idx)                                                                            \
+    do {                                                                                            \
+        if (a.trace && blockIdx.x == 0 && (int64_t)(idx) < a.trace_n) a.trace[(int64_t)(idx) * 16 + (slot)] = clock64(); \
+    } while (0)
+
 // Warp-specialised persistent kernel, one CTA per SM:
-//   warps 0-3  producers: one TMA load of the group's query rows (B, all K,
-//              resident for the whole item) + bit -> byte expansion of each
-//              code tile (A) into a 4-stage shared-memory ring
-//   warp 4     MMA issuer: 4 UMMA (K = 32 each) per 128-byte chunk into one of
+//   warps 0-7  producers: thread (g, r) expands code words 4c+2g, 4c+2g+1 of
+//              vector row r for every K chunk c into the A ring (code words
+//              prefetched one tile ahead in registers)
+//   warp 8     MMA issuer: 4 UMMA (K = 32 each) per 128-byte chunk into one of
 //              two TMEM accumulators per vector tile; tcgen05.commit frees A
-//              stages, publishes accumulators and frees B after the item
-//   warps 5-12 epilogue: tcgen05.ld the int32 inner products, fused
+//              stages, publishes accumulators and frees each B chunk after the
+//              item's last tile used it
+//   warp 9     query loader: TMA of the group's int8 query rows (B, resident per
+//              item), chunk c of the next item as soon as chunk c is free
+//   warps 10-17 epilogue: tcgen05.ld the int32 inner products, fused
 //              estimator (+ bound), threshold, survivor append
 template <bool kLB, bool kDump, bool kRetry>
 __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant__ CUtensorMap tmapB, ScanArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-    uint8_t* Bres = smem;                    // [nchunks][NG rows][128 B], 128-byte swizzle
-    uint8_t* stA = smem + kBRes;             // [kStages][kStageA]
-    uint32_t* raw = reinterpret_cast<uint32_t*>(stA + kStages * kStageA);  // [2][128 x W] raw code tiles
-    __shared__ __align__(16) ColC colc[2 * kTN];
-    __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], accf_bar[2], acce_bar[2], bfull_bar,
-        bfree_bar, raw_bar[2];
+    const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
+    uint8_t* smem = smem_raw + pad;
+    const SmemPlan sp = smem_plan(a.Dp);
+    uint8_t* Bres = smem;                                        // [nchunks][NG rows][128 B], 128-byte swizzle
+    ColC* colc = reinterpret_cast<ColC*>(smem + sp.off_colc);    // [2][NG]
+    uint8_t* stA = smem + sp.off_A;                              // [stages][kStageA]
+    __shared__ __align__(8) uint64_t full_bar[kMaxStages], empty_bar[kMaxStages], accf_bar[2], acce_bar[2],
+        bfull_bar[kMaxChunks], bfree_bar[kMaxChunks];
     __shared__ uint32_t tmem_base_s;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nchunks = sp.nchunks, NG = sp.NG, nst = sp.stages;
     if (warp == kMmaWarp) tc::tmem_alloc(&tmem_base_s, kTmemCols);
     if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < nst; ++s) {
             tc::mbar_init(&full_bar[s], 1);
             tc::mbar_init(&empty_bar[s], 1);
         }
@@ -138,10 +182,10 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
             tc::mbar_init(&accf_bar[b], 1);
             tc::mbar_init(&acce_bar[b], kEpiWarps);
         }
-        tc::mbar_init(&bfull_bar, 1);
-        tc::mbar_init(&bfree_bar, 1);
-        tc::mbar_init(&raw_bar[0], 1);
-        tc::mbar_init(&raw_bar[1], 1);
+        for (int c = 0; c < nchunks; ++c) {
+            tc::mbar_init(&bfull_bar[c], 1);
+            tc::mbar_init(&bfree_bar[c], 1);
+        }
         tc::prefetch_tmap(&tmapB);
     }
     tc::fence_before_sync();
@@ -150,93 +194,98 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
     const uint32_t tmem = tmem_base_s;
 
     const int64_t total = a.list_items[a.nlist];
-    const int nchunks = (a.Dp + kKC - 1) / kKC;
-    const int NG = group_cols(a.Dp);
-    const int bchunk = NG * kKC;             // bytes of one K chunk of the resident B
+    const int bchunk = NG * kKC;  // bytes of one K chunk of the resident B
 
     if (warp < kProdWarps) {
         // ================= producers =================
-        // raw code tiles (128 x W words, contiguous) arrive by bulk copy one tile
-        // ahead into a 2-buffer ring; each thread expands its row chunk by chunk
-        const int r = tid;  // tile row 0..127 = vector
-        const uint32_t raw_bytes = (uint32_t)(kTM * a.W * 4);
-        uint32_t gc = 0, ic = 0, rc = 0;  // chunk, item, raw-tile counters
-        int64_t item = blockIdx.x;
-        Item it{};
-        if (item < total) it = decode_item(a, NG, item);
-        // (item, tile) of the raw tile to prefetch next
-        int64_t pf_item = item;
-        Item pf_it = it;
-        int pf_t = 0;
-        auto issue_raw = [&](uint32_t k) {  // bulk copy of the next tile into raw buffer k & 1
-            if (pf_item >= total) return;
-            if (tid == 0) {
-                const int64_t slot0 = pf_it.slot_base + (pf_it.t0 + pf_t) * kTM;  // multiple of 32
-                tc::mbar_arrive_expect_tx(&raw_bar[k & 1], raw_bytes);
-                tc::bulk_load(raw + (k & 1) * (kRawMax / 4), a.codes + (size_t)(slot0 >> 5) * a.W * 32, raw_bytes,
-                              &raw_bar[k & 1]);
-            }
-            if (++pf_t >= pf_it.ntiles) {
-                pf_t = 0;
-                pf_item += gridDim.x;
-                if (pf_item < total) pf_it = decode_item(a, NG, pf_item);
+        const int r = tid & (kTM - 1);  // tile row = vector
+        const int g = tid >> 7;         // word group: words 4c + 2g, 4c + 2g + 1 of chunk c
+        const int W = a.W;
+        // code words of this thread for one tile, k-th = word 4 (k >> 1) + 2 g + (k & 1)
+        auto load_tile = [&](const Item& it, int t, uint32_t (&w)[kWPT]) {
+            const int64_t slot = it.slot_base + (it.t0 + t) * kTM + r;  // slot_base multiple of 32
+            const uint32_t* src = a.codes + (size_t)(slot >> 5) * W * 32 + (slot & 31);
+#pragma unroll
+            for (int k = 0; k < kWPT; ++k) {
+                const int wd = 4 * (k >> 1) + 2 * g + (k & 1);
+                w[k] = wd < W ? __ldg(src + (size_t)wd * 32) : 0u;
             }
         };
-        issue_raw(0);
-        for (; item < total; item += gridDim.x, ++ic) {
-            if (tid == 0) {
-                if (ic > 0) tc::mbar_wait(&bfree_bar, (ic - 1) & 1);  // previous item's UMMAs retired
-                tc::mbar_arrive_expect_tx(&bfull_bar, (uint32_t)(it.nboxes * nchunks * kBoxRows * kKC));
-                for (int c = 0; c < nchunks; ++c)
-                    for (int bx = 0; bx < it.nboxes; ++bx)
-                        tc::tma_load_2d(Bres + c * bchunk + bx * kBoxRows * kKC, &tmapB, &bfull_bar, c * kKC,
-                                        (int)(it.grow0 + bx * kBoxRows));
-            }
-            for (int t = 0; t < it.ntiles; ++t, ++rc) {
-                issue_raw(rc + 1);  // the other buffer was released by the barrier ending tile rc - 1
-                tc::mbar_wait(&raw_bar[rc & 1], (rc >> 1) & 1);
-                const uint32_t* rt = raw + (rc & 1) * (kRawMax / 4) + (r >> 5) * a.W * 32 + (r & 31);
-                for (int c = 0; c < nchunks; ++c, ++gc) {
-                    const int s = gc % kStages;
-                    const uint32_t u = gc / kStages;
-                    const int kbytes = min(kKC, a.Dp - c * kKC);
+        uint32_t cur[kWPT], nxt[kWPT];
+        uint32_t gc = 0;
+        int64_t item = blockIdx.x;
+        Item it{};
+        if (item < total) {
+            it = decode_item(a, NG, item);
+            load_tile(it, 0, cur);
+        }
+        for (; item < total; item += gridDim.x) {
+            const int64_t nitem = item + gridDim.x;
+            Item nit{};
+            if (nitem < total) nit = decode_item(a, NG, nitem);
+            for (int t = 0; t < it.ntiles; ++t) {
+                // prefetch the next tile's code words (consumed after this tile)
+                if (t + 1 < it.ntiles) load_tile(it, t + 1, nxt);
+                else if (nitem < total) load_tile(nit, 0, nxt);
+#pragma unroll
+                for (int c = 0; c < kMaxChunks; ++c) {
+                    if (c >= nchunks) break;
+                    const int s = gc % nst;
+                    const uint32_t u = gc / nst;
+                    ++gc;
+                    if (tid == 0) RQ_TR(0, gc - 1);
                     if (u > 0) tc::mbar_wait(&empty_bar[s], (u - 1) & 1);
+                    if (tid == 0) RQ_TR(1, gc - 1);
+                    if (tid == 128) RQ_TR(5, gc - 1);
                     uint8_t* A = stA + s * kStageA + (r >> 3) * kSBO + (r & 7) * 16;
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        if (q * 32 >= kbytes) break;
-                        const uint32_t x = rt[(c * 4 + q) * 32];
-                        *reinterpret_cast<uint4*>(A + (2 * q) * 128) = expand16(x & 0xFFFFu);
-                        *reinterpret_cast<uint4*>(A + (2 * q + 1) * 128) = expand16(x >> 16);
+                    for (int h = 0; h < 2; ++h) {
+                        const int qw = 2 * g + h;  // word within the chunk
+                        if (4 * c + qw < W) {
+                            uint4 lo, hi;
+                            expand32(cur[2 * c + h], lo, hi);
+                            *reinterpret_cast<uint4*>(A + (2 * qw) * 128) = lo;
+                            *reinterpret_cast<uint4*>(A + (2 * qw + 1) * 128) = hi;
+                        }
                     }
+                    if (tid == 0) RQ_TR(2, gc - 1);
                     tc::fence_proxy_async();
-                    tc::named_barrier(2, kProdWarps * 32);  // stage written (also releases the raw buffer after the last chunk)
+                    if (tid == 0) RQ_TR(3, gc - 1);
+                    tc::named_barrier(2, kProdWarps * 32);  // stage written by all producers
                     if (tid == 0) tc::mbar_arrive(&full_bar[s]);
+                    if (tid == 0) RQ_TR(4, gc - 1);
+                    if (tid == 128) RQ_TR(6, gc - 1);
                 }
+#pragma unroll
+                for (int k = 0; k < kWPT; ++k) cur[k] = nxt[k];
             }
-            if (item + gridDim.x < total) it = decode_item(a, NG, item + gridDim.x);
+            it = nit;
         }
     } else if (warp == kMmaWarp) {
         // ================= MMA issuer =================
         uint32_t gc = 0, tcnt = 0, ic = 0;
         for (int64_t item = blockIdx.x; item < total; item += gridDim.x, ++ic) {
             const Item it = decode_item(a, NG, item);
-            const uint32_t idesc = tc::idesc_i8(kTM, it.ncols16);
-            tc::mbar_wait(&bfull_bar, ic & 1);
-            tc::fence_after_sync();
+            const uint32_t idesc = tc::idesc_i8(kTM, it.ncols16, /*a_signed=*/true);
             const uint32_t baddr = tc::smem_u32(Bres);
             for (int t = 0; t < it.ntiles; ++t, ++tcnt) {
                 const int b = tcnt & 1;
                 const uint32_t ub = tcnt >> 1;
+                if (lane == 0) RQ_TR(11, tcnt);
                 if (ub > 0) tc::mbar_wait(&acce_bar[b], (ub - 1) & 1);
+                if (lane == 0) RQ_TR(12, tcnt);
                 tc::fence_after_sync();
                 const uint32_t dacc = tmem + (uint32_t)(b * kTN);
                 for (int c = 0; c < nchunks; ++c, ++gc) {
-                    const int s = gc % kStages;
-                    const uint32_t u = gc / kStages;
+                    const int s = gc % nst;
+                    const uint32_t u = gc / nst;
                     const int kbytes = min(kKC, a.Dp - c * kKC);
+                    if (lane == 0) RQ_TR(7, gc);
+                    if (t == 0) tc::mbar_wait(&bfull_bar[c], ic & 1);
+                    if (lane == 0) RQ_TR(8, gc);
                     tc::mbar_wait(&full_bar[s], u & 1);
                     tc::fence_after_sync();
+                    if (lane == 0) RQ_TR(9, gc);
                     if (lane == 0) {
                         const uint32_t aaddr = tc::smem_u32(stA + s * kStageA);
                         const int nks = (a.experiment & 2) ? ((c == 0) ? 1 : 0) : kbytes / 32;
@@ -245,14 +294,29 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                             const uint64_t bd = tc::smem_desc_sw128(baddr + c * bchunk + ks * 32);
                             tc::mma_i8(dacc, ad, bd, idesc, (c > 0 || ks > 0) ? 1u : 0u);
                         }
-                        tc::commit(&empty_bar[s]);                       // A stage s free once these retire
-                        if (c == nchunks - 1) tc::commit(&accf_bar[b]);  // accumulator b complete
+                        tc::commit(&empty_bar[s]);                          // A stage s free once these retire
+                        if (t == it.ntiles - 1) tc::commit(&bfree_bar[c]);  // B chunk c free for the next item
+                        if (c == nchunks - 1) tc::commit(&accf_bar[b]);     // accumulator b complete
+                        RQ_TR(10, gc);
                     }
                     __syncwarp();
                 }
             }
-            if (lane == 0) tc::commit(&bfree_bar);  // resident B free once the item's UMMAs retire
-            __syncwarp();
+        }
+    } else if (warp == kLoadWarp) {
+        // ================= query operand loader =================
+        if (lane == 0) {
+            uint32_t ic = 0;
+            for (int64_t item = blockIdx.x; item < total; item += gridDim.x, ++ic) {
+                const Item it = decode_item(a, NG, item);
+                for (int c = 0; c < nchunks; ++c) {
+                    if (ic > 0) tc::mbar_wait(&bfree_bar[c], (ic - 1) & 1);  // previous item done with chunk c
+                    tc::mbar_arrive_expect_tx(&bfull_bar[c], (uint32_t)(it.nboxes * kBoxRows * kKC));
+                    for (int bx = 0; bx < it.nboxes; ++bx)
+                        tc::tma_load_2d(Bres + c * bchunk + bx * kBoxRows * kKC, &tmapB, &bfull_bar[c], c * kKC,
+                                        (int)(it.grow0 + bx * kBoxRows));
+                }
+            }
         }
     } else {
         // ================= epilogue =================
@@ -265,7 +329,7 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
         int64_t item = blockIdx.x;
         Item it{};
         ColC nextc;
-        auto fetch_colc = [&](const Item& x) {  // one coalesced 32-byte load per column
+        auto fetch_colc = [&](const Item& x) {  // one coalesced 32-byte load per column (NG <= 256)
             if (et < x.ncols) {
                 nextc = a.gcolc[x.grow0 + et];
             } else {
@@ -279,12 +343,11 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
         if (item < total) {
             it = decode_item(a, NG, item);
             fetch_colc(it);
-            colc[et] = nextc;
+            if (et < NG) colc[et] = nextc;
         }
         tc::named_barrier(1, kEpiWarps * 32);
         for (; item < total; item += gridDim.x, ++ic) {
-            const int cbuf = ic & 1;
-            const ColC* cb = colc + cbuf * kTN;
+            const ColC* cb = colc + (ic & 1) * NG;
             // prefetch the next item's column constants (latency hidden by this item)
             const int64_t nitem = item + gridDim.x;
             Item nit{};
@@ -299,10 +362,12 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                 const bool vok = v < it.L;
                 const int64_t slot = it.slot_base + v;
                 const float2 fac = vok ? a.fac[slot] : make_float2(0.f, 0.f);
-                const int pc = vok ? (int)a.pcnt[slot] : 0;
+                const float pcf = vok ? (float)a.pcnt[slot] : 0.f;
                 const float g1 = (kLB && vok) ? a.g1[slot] : 0.f;
                 const uint32_t row = vok ? a.rows[slot] : 0u;
+                if (e == 0 && lane == 0) RQ_TR(13, tcnt);
                 tc::mbar_wait(&accf_bar[b], ub & 1);
+                if (e == 0 && lane == 0) RQ_TR(14, tcnt);
                 tc::fence_after_sync();
 #pragma unroll 1
                 for (int hc = half; hc * 32 < ((a.experiment & 1) ? 0 : it.ncols); hc += 2) {
@@ -315,20 +380,23 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
                         const ColC& cc = cb[col0 + i];  // empty columns have tau = -inf
-                        const int ip = (int)acc[i];
-                        const float est = rabitq_est(ip, pc, fac, cc.c);
+                        // acc = -ip (s8 codes in {0, -1}); 0x4B400000 + n is the float
+                        // 1.5 2^23 + n exactly for |n| < 2^22, so ipn = -ip exactly
+                        const float ipn = __fsub_rn(__int_as_float(0x4B400000 + (int)acc[i]), 12582912.0f);
+                        const float tt = __fmaf_rn(-cc.c.a, ipn, __fmaf_rn(cc.c.b, pcf, -cc.c.K));
+                        const float est = __fmaf_rn(-fac.y, tt, __fadd_rn(fac.x, cc.c.nq2));
                         key[i] = rank_key<kLB>(est, cc.epsnq, g1);
                         if constexpr (kDump) {
                             if (vok && col0 + i < it.ncols) {
                                 const int64_t di = (a.item_off[cc.pair] + (v >> 5)) * 32 + (v & 31);
                                 if (di < a.dump_cap) {
-                                    a.dump_ip[di] = ip;
+                                    a.dump_ip[di] = -(int)acc[i];
                                     a.dump_est[di] = est;
                                 }
                             }
                         }
                         bool sv;
-                        if constexpr (kRetry) {  // exact (key, row) <= tau64 (overflow re-scan)
+                        if constexpr (kRetry) {  // exact (key, row) <= tau64 (overflow / underflow re-scan)
                             const uint32_t ko = f2o(key[i]), to = f2o(cc.tau);
                             sv = vok && (ko < to || (ko == to && row <= (uint32_t)cc.pair));
                         } else {
@@ -357,10 +425,11 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                 tc::fence_before_sync();
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&acce_bar[b]);  // accumulator b may be overwritten
+                if (e == 0 && lane == 0) RQ_TR(15, tcnt);
             }
-            // publish the next item's column constants into the other buffer (its last
-            // readers finished item ic - 1 before the previous barrier)
-            if (nitem < total) colc[(cbuf ^ 1) * kTN + et] = nextc;
+            // publish the next item's column constants into the other buffer (its
+            // last readers finished item ic - 1 before the previous barrier)
+            if (nitem < total && et < NG) colc[((ic + 1) & 1) * NG + et] = nextc;
             tc::named_barrier(1, kEpiWarps * 32);
             it = nit;
         }
@@ -454,7 +523,7 @@ __global__ void list_items_kernel(int nlist, const int64_t* __restrict__ list_of
 
 bool imma_wanted(const rabitq_index* idx, int64_t npairs, int scan_path) {
     if (scan_path == RABITQ_SCAN_POPC) return false;
-    if (idx->W > kRawMax / (128 * 4)) return false;  // raw code tile must fit its smem buffer (D <= 960)
+    if (idx->W > 2 * kWPT || idx->W > 4 * kMaxChunks) return false;  // producer registers / B chunks (D <= 1024)
     if (scan_path == RABITQ_SCAN_IMMA) return true;
     // AUTO: the tensor-core path pays once lists are shared by enough queries
     return npairs >= (int64_t)8 * idx->nlist;
@@ -551,7 +620,9 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
                                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     RQ_REQUIRE(cr == CUDA_SUCCESS, RABITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
-    const size_t smem = 1024 + (size_t)kBRes + (size_t)kStages * kStageA + 2 * (size_t)kRawMax;
+    const SmemPlan plan = smem_plan(a.Dp);
+    RQ_REQUIRE(plan.stages >= 2, RABITQ_ERR_INTERNAL, "grouped scan: shared-memory plan has < 2 stages");
+    const size_t smem = plan.total;
     const int grid = sms;
 #define RQ_IMMA(LB, DP, RT)                                                                                     \
     do {                                                                                                        \

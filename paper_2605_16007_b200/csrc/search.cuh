@@ -47,6 +47,8 @@ struct ScanArgs {
     const uint16_t* pcnt;      // [nslots] popcount of each code
     const ColC* gcolc;         // [npairs] column constants in grouped order
     int experiment;            // diagnostics (RABITQ_IMMA_EXPERIMENT): 1 skip epilogue math, 2 skip UMMAs
+    long long* trace;          // diagnostics (RABITQ_SCAN_TRACE): clock64 stamps of CTA 0, [trace_n][16]
+    int trace_n;
 };
 
 template <typename T>
@@ -97,6 +99,7 @@ struct RerankArgs {
     int nprobe;
     const float4* qscal;
     const float* g1;
+    const int32_t* order;      // [nq] block -> query (queries sharing their nearest list run together)
 };
 
 struct SearchCfg {

@@ -112,10 +112,11 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
     return d;
 }
 
-// Instruction descriptor, .kind::i8: D = s32, A = u8, B = u8, both K-major.
-__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+// Instruction descriptor, .kind::i8: D = s32, A = u8 or s8, B = u8, both K-major.
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N, bool a_signed = false) {
     return (2u << 4)                       // c_format: S32
-           | (0u << 7) | (0u << 10)        // a/b format: unsigned 8-bit
+           | ((a_signed ? 1u : 0u) << 7)   // a format: 0 unsigned / 1 signed 8-bit
+           | (0u << 10)                    // b format: unsigned 8-bit
            | (0u << 15) | (0u << 16)       // a/b major: K
            | ((uint32_t)(N >> 3) << 17)    // N / 8
            | ((uint32_t)(M >> 4) << 24);   // M / 16
