@@ -39,47 +39,49 @@ namespace rabitq {
 namespace {
 
 constexpr int kTM = 128;                   // vectors per tile (UMMA M)
-constexpr int kTN = 256;                   // max queries per group (max UMMA N); grouped-row padding
+constexpr int kTN = 256;                   // grouped-row padding (>= max group size)
 constexpr int kKC = 128;                   // bytes of K per chunk (one 128-byte swizzle row of B)
+constexpr int kChunkCols = kKC / 4;        // TMEM columns of one A chunk (4 int8 per column)
 constexpr int kMaxChunks = 8;              // Dp <= 1024
-constexpr int kMaxStages = 10;             // A (expanded code) ring, sized from the shared-memory budget
-constexpr int kStageA = kTM * kKC;         // 16 KB, canonical no-swizzle K-major
-constexpr int kBRes = 128 * 1024;          // resident query operand (all K chunks of one group)
-constexpr int kSBO = (kKC / 16) * 128;     // A: distance between 8-row core-matrix groups
+constexpr int kMaxSlots = 8;               // A ring slots in TMEM
+constexpr int kBRes = 192 * 1024;          // resident query operand (all K chunks of one group)
+constexpr int kMaxNG = 224;                // 2 NG accumulator columns + >= 2 A slots <= 512
 constexpr int kBoxRows = 32;               // TMA box = 32 query rows x 128 bytes
 constexpr int kTilesPerItem = 8;           // vector tiles per work item (B loaded once per item)
-constexpr int kProdWarps = 8;              // two groups of 4: group g expands words 4c+2g, 4c+2g+1 of chunk c
-constexpr int kMmaWarp = kProdWarps;       // warp 8 issues the UMMAs (and owns TMEM)
-constexpr int kLoadWarp = kProdWarps + 1;  // warp 9 streams the query operand (TMA)
-constexpr int kEpiWarp0 = kProdWarps + 2;  // warps 10..17
+constexpr int kProdWarps = 4;              // thread r expands code row r into TMEM lane r
+constexpr int kMmaWarp = kProdWarps;       // warp 4 issues the UMMAs (and owns TMEM)
+constexpr int kLoadWarp = kProdWarps + 1;  // warp 5 streams the query operand (TMA)
+constexpr int kEpiWarp0 = kProdWarps + 2;  // warps 6..13
 constexpr int kEpiWarps = 8;
-constexpr int kNT = (kEpiWarp0 + kEpiWarps) * 32;  // 576 threads
-constexpr int kTmemCols = 2 * kTN;         // double-buffered accumulator: 512 columns
-constexpr int kWPT = 16;                   // max code words per producer thread and tile (W <= 30)
+constexpr int kNT = (kEpiWarp0 + kEpiWarps) * 32;  // 448 threads: <= 4 warps per SMSP -> 128 registers
+constexpr int kTmemCols = 512;
+constexpr int kPF = 8;                     // code-word prefetch ring (chunks in flight per producer thread)
 constexpr int kSmemLimit = 227 * 1024;
 
-// queries per group so that all K chunks of a group fit the resident B region
+// queries per group: all K chunks of a group fit the resident B region, and
+// the double-buffered accumulator leaves TMEM room for >= 2 A slots
 __host__ __device__ inline int group_cols(int Dp) {
     const int nch = (Dp + kKC - 1) / kKC;
     int n = (kBRes / (nch * kKC)) / kBoxRows * kBoxRows;
-    return n > kTN ? kTN : n;
+    return n > kMaxNG ? kMaxNG : n;
 }
 
-// shared-memory plan of one launch (host and device agree)
+// shared-memory / TMEM plan of one launch (host and device agree)
 struct SmemPlan {
-    int nchunks, NG, stages;
-    uint32_t off_colc, off_A, total;
+    int nchunks, NG, slots;
+    uint32_t acc_cols, off_colc, off_raw, total;
 };
 __host__ __device__ inline SmemPlan smem_plan(int Dp) {
     SmemPlan p;
     p.nchunks = (Dp + kKC - 1) / kKC;
     p.NG = group_cols(Dp);
+    p.acc_cols = (uint32_t)((p.NG + 31) & ~31);  // per accumulator buffer
+    int slots = (kTmemCols - 2 * (int)p.acc_cols) / kChunkCols;
+    p.slots = slots < kMaxSlots ? slots : kMaxSlots;
     const uint32_t bres = (uint32_t)(p.nchunks * p.NG * kKC);
-    p.off_colc = bres;                                      // [2][NG] ColC
-    p.off_A = ((p.off_colc + 2u * p.NG * (uint32_t)sizeof(ColC)) + 1023u) & ~1023u;
-    const int room = (kSmemLimit - 1024 - 2048 - (int)p.off_A) / kStageA;  // 1 KB align slack, 2 KB static
-    p.stages = room < kMaxStages ? room : kMaxStages;
-    p.total = p.off_A + (uint32_t)p.stages * kStageA + 1024u;
+    p.off_colc = bres;  // [2][NG] ColC
+    p.off_raw = p.off_colc + 2u * p.NG * (uint32_t)sizeof(ColC);  // [kPF][128 rows][4 words]
+    p.total = p.off_raw + (uint32_t)(kPF * kTM * 16) + 1024u;
     return p;
 }
 
@@ -121,7 +123,7 @@ __device__ __forceinline__ Item decode_item(const ScanArgs& a, int NG, int64_t i
 // 32 code bits -> 32 bytes in {0, -1} (s8), K order permuted: output byte
 // k = 4 s + t (s = 0..7, t = 0..3) holds code bit 8 t + 7 - s, the sign bit of
 // byte t of (x << s), replicated by PRMT.  The quantizer writes the query rows
-// in the same K order (kperm_dim), so the contraction is unchanged:
+// in the same K order, so the contraction is unchanged:
 //   sum_k A[k] B[k] = - sum_i b_i qbar_i = -ip.
 __device__ __forceinline__ uint32_t sgnrep(uint32_t y) {
     uint32_t r;
@@ -139,23 +141,56 @@ __device__ __forceinline__ void expand32(uint32_t x, uint4& lo, uint4& hi) {
     hi.w = sgnrep(x * 128u);
 }
 
+// fused estimator from the accumulator (acc = -ip: s8 codes in {0, -1}).
+// 0x4B400000 + n is the float 1.5 2^23 + n exactly for |n| < 2^22, so ipn = -ip
+// exactly; the rest is rabitq_est's arithmetic (a ip = (-a)(-ip) exactly).
+__device__ __forceinline__ float est_of(uint32_t acc, const ColC& cc, float2 fac, float pcf) {
+    const float ipn = __fsub_rn(__int_as_float(0x4B400000 + (int)acc), 12582912.0f);
+    const float tt = __fmaf_rn(-cc.c.a, ipn, __fmaf_rn(cc.c.b, pcf, -cc.c.K));
+    return __fmaf_rn(-fac.y, tt, __fadd_rn(fac.x, cc.c.nq2));
+}
+
 // clock stamps of CTA 0 (RABITQ_SCAN_TRACE diagnostics): row idx, column slot
+// (compiled in with -DRABITQ_SCAN_TRACE only; the stamps cost issue slots)
+#ifdef RABITQ_SCAN_TRACE
 #define RQ_TR(slot, idx)                                                                            \
     do {                                                                                            \
         if (a.trace && blockIdx.x == 0 && (int64_t)(idx) < a.trace_n) a.trace[(int64_t)(idx) * 16 + (slot)] = clock64(); \
     } while (0)
+#else
+#define RQ_TR(slot, idx) \
+    do {                 \
+    } while (0)
+#endif
 
-// Warp-specialised persistent kernel, one CTA per SM:
-//   warps 0-7  producers: thread (g, r) expands code words 4c+2g, 4c+2g+1 of
-//              vector row r for every K chunk c into the A ring (code words
-//              prefetched one tile ahead in registers)
-//   warp 8     MMA issuer: 4 UMMA (K = 32 each) per 128-byte chunk into one of
-//              two TMEM accumulators per vector tile; tcgen05.commit frees A
-//              stages, publishes accumulators and frees each B chunk after the
-//              item's last tile used it
-//   warp 9     query loader: TMA of the group's int8 query rows (B, resident per
+// position of one K chunk in a CTA's work sequence (items strided by the grid)
+struct Pos {
+    int64_t item;
+    Item it;
+    int t, c;
+};
+__device__ __forceinline__ void pos_next(const ScanArgs& a, int NG, int nchunks, int64_t total, Pos& p) {
+    if (++p.c < nchunks) return;
+    p.c = 0;
+    if (++p.t < p.it.ntiles) return;
+    p.t = 0;
+    p.item += gridDim.x;
+    if (p.item < total) p.it = decode_item(a, NG, p.item);
+}
+
+// Warp-specialised persistent kernel, one CTA per SM.  TMEM (512 columns):
+// two int32 accumulators of acc_cols columns + a ring of A slots (32 columns =
+// one 128-byte K chunk of a 128-vector code tile each).
+//   warps 0-3  producers: thread r expands code row r chunk by chunk (PRMT, see
+//              expand32) straight into TMEM lane r of the next A slot
+//              (tcgen05.st; code words prefetched two chunks ahead)
+//   warp 4     MMA issuer: 4 UMMA (A from TMEM, B from shared memory, K = 32
+//              each) per chunk into one of two accumulators per vector tile;
+//              tcgen05.commit frees A slots, publishes accumulators and frees
+//              each B chunk after the item's last tile used it
+//   warp 5     query loader: TMA of the group's int8 query rows (B, resident per
 //              item), chunk c of the next item as soon as chunk c is free
-//   warps 10-17 epilogue: tcgen05.ld the int32 inner products, fused
+//   warps 6-13 epilogue: tcgen05.ld the int32 inner products, fused
 //              estimator (+ bound), threshold, survivor append
 template <bool kLB, bool kDump, bool kRetry>
 __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant__ CUtensorMap tmapB, ScanArgs a) {
@@ -165,16 +200,15 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
     const SmemPlan sp = smem_plan(a.Dp);
     uint8_t* Bres = smem;                                        // [nchunks][NG rows][128 B], 128-byte swizzle
     ColC* colc = reinterpret_cast<ColC*>(smem + sp.off_colc);    // [2][NG]
-    uint8_t* stA = smem + sp.off_A;                              // [stages][kStageA]
-    __shared__ __align__(8) uint64_t full_bar[kMaxStages], empty_bar[kMaxStages], accf_bar[2], acce_bar[2],
+    __shared__ __align__(8) uint64_t full_bar[kMaxSlots], empty_bar[kMaxSlots], accf_bar[2], acce_bar[2],
         bfull_bar[kMaxChunks], bfree_bar[kMaxChunks];
     __shared__ uint32_t tmem_base_s;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int nchunks = sp.nchunks, NG = sp.NG, nst = sp.stages;
+    const int nchunks = sp.nchunks, NG = sp.NG, nsl = sp.slots;
     if (warp == kMmaWarp) tc::tmem_alloc(&tmem_base_s, kTmemCols);
     if (tid == 0) {
-        for (int s = 0; s < nst; ++s) {
+        for (int s = 0; s < nsl; ++s) {
             tc::mbar_init(&full_bar[s], 1);
             tc::mbar_init(&empty_bar[s], 1);
         }
@@ -192,82 +226,82 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = tmem_base_s;
+    const uint32_t tmemA = tmem + 2u * sp.acc_cols;  // A slot s at columns tmemA + 32 s
 
     const int64_t total = a.list_items[a.nlist];
     const int bchunk = NG * kKC;  // bytes of one K chunk of the resident B
 
     if (warp < kProdWarps) {
         // ================= producers =================
-        const int r = tid & (kTM - 1);  // tile row = vector
-        const int g = tid >> 7;         // word group: words 4c + 2g, 4c + 2g + 1 of chunk c
+        const int r = tid;  // tile row = vector = TMEM lane
         const int W = a.W;
-        // code words of this thread for one tile, k-th = word 4 (k >> 1) + 2 g + (k & 1)
-        auto load_tile = [&](const Item& it, int t, uint32_t (&w)[kWPT]) {
-            const int64_t slot = it.slot_base + (it.t0 + t) * kTM + r;  // slot_base multiple of 32
-            const uint32_t* src = a.codes + (size_t)(slot >> 5) * W * 32 + (slot & 31);
+        const uint32_t lane_addr = (uint32_t)(warp * 32) << 16;
+        uint32_t* raw = reinterpret_cast<uint32_t*>(smem + sp.off_raw);  // [kPF][128][4]
+        // this thread's 4 code words of chunk p -> ring entry e (async, zero-filled past W)
+        auto issue = [&](const Pos& p, int e) {
+            if (p.item < total) {
+                const int64_t slot = p.it.slot_base + (p.it.t0 + p.t) * kTM + r;  // slot_base multiple of 32
+                const uint32_t* src = a.codes + (size_t)(slot >> 5) * W * 32 + (slot & 31);
 #pragma unroll
-            for (int k = 0; k < kWPT; ++k) {
-                const int wd = 4 * (k >> 1) + 2 * g + (k & 1);
-                w[k] = wd < W ? __ldg(src + (size_t)wd * 32) : 0u;
-            }
-        };
-        uint32_t cur[kWPT], nxt[kWPT];
-        uint32_t gc = 0;
-        int64_t item = blockIdx.x;
-        Item it{};
-        if (item < total) {
-            it = decode_item(a, NG, item);
-            load_tile(it, 0, cur);
-        }
-        for (; item < total; item += gridDim.x) {
-            const int64_t nitem = item + gridDim.x;
-            Item nit{};
-            if (nitem < total) nit = decode_item(a, NG, nitem);
-            for (int t = 0; t < it.ntiles; ++t) {
-                // prefetch the next tile's code words (consumed after this tile)
-                if (t + 1 < it.ntiles) load_tile(it, t + 1, nxt);
-                else if (nitem < total) load_tile(nit, 0, nxt);
-#pragma unroll
-                for (int c = 0; c < kMaxChunks; ++c) {
-                    if (c >= nchunks) break;
-                    const int s = gc % nst;
-                    const uint32_t u = gc / nst;
-                    ++gc;
-                    if (tid == 0) RQ_TR(0, gc - 1);
-                    if (u > 0) tc::mbar_wait(&empty_bar[s], (u - 1) & 1);
-                    if (tid == 0) RQ_TR(1, gc - 1);
-                    if (tid == 128) RQ_TR(5, gc - 1);
-                    uint8_t* A = stA + s * kStageA + (r >> 3) * kSBO + (r & 7) * 16;
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int qw = 2 * g + h;  // word within the chunk
-                        if (4 * c + qw < W) {
-                            uint4 lo, hi;
-                            expand32(cur[2 * c + h], lo, hi);
-                            *reinterpret_cast<uint4*>(A + (2 * qw) * 128) = lo;
-                            *reinterpret_cast<uint4*>(A + (2 * qw + 1) * 128) = hi;
-                        }
-                    }
-                    if (tid == 0) RQ_TR(2, gc - 1);
-                    tc::fence_proxy_async();
-                    if (tid == 0) RQ_TR(3, gc - 1);
-                    tc::named_barrier(2, kProdWarps * 32);  // stage written by all producers
-                    if (tid == 0) tc::mbar_arrive(&full_bar[s]);
-                    if (tid == 0) RQ_TR(4, gc - 1);
-                    if (tid == 128) RQ_TR(6, gc - 1);
+                for (int k = 0; k < 4; ++k) {
+                    const int wd = 4 * p.c + k;
+                    tc::cp_async4(raw + (e * kTM + r) * 4 + k, src + (size_t)min(wd, W - 1) * 32, wd < W ? 4u : 0u);
                 }
-#pragma unroll
-                for (int k = 0; k < kWPT; ++k) cur[k] = nxt[k];
             }
-            it = nit;
+            tc::cp_async_commit();  // (possibly empty) group per chunk keeps the wait count uniform
+        };
+        Pos pf{(int64_t)blockIdx.x, Item{}, 0, 0};
+        if (pf.item < total) pf.it = decode_item(a, NG, pf.item);
+        Pos cur = pf;
+        for (int i = 0; i < kPF - 1; ++i) {
+            issue(pf, i);
+            pos_next(a, NG, nchunks, total, pf);
         }
+        int s = 0, e = 0;
+        uint32_t u = 0;
+        for (uint32_t gc = 0; cur.item < total; ++gc) {
+            issue(pf, (e + kPF - 1) % kPF);  // kPF - 1 chunks ahead
+            pos_next(a, NG, nchunks, total, pf);
+            tc::cp_async_wait<kPF - 1>();  // this thread's words of chunk gc have landed
+            const uint4 wv = *reinterpret_cast<const uint4*>(raw + (e * kTM + r) * 4);
+            if (tid == 0) RQ_TR(0, gc);
+            if (u > 0) tc::mbar_wait(&empty_bar[s], (u - 1) & 1);
+            tc::fence_after_sync();
+            if (tid == 0) RQ_TR(1, gc);
+            const uint32_t dst = tmemA + (uint32_t)(s * kChunkCols) + lane_addr;
+            uint4 lo, hi;
+            expand32(wv.x, lo, hi);
+            tc::tmem_st8(dst, lo, hi);
+            expand32(wv.y, lo, hi);
+            tc::tmem_st8(dst + 8, lo, hi);
+            expand32(wv.z, lo, hi);
+            tc::tmem_st8(dst + 16, lo, hi);
+            expand32(wv.w, lo, hi);
+            tc::tmem_st8(dst + 24, lo, hi);
+            tc::tmem_st_wait();
+            tc::fence_before_sync();
+            if (tid == 0) RQ_TR(2, gc);
+            tc::named_barrier(2, kProdWarps * 32);  // slot written by all 128 rows
+            if (tid == 0) {
+                tc::mbar_arrive(&full_bar[s]);
+                RQ_TR(4, gc);
+            }
+            if (++s == nsl) {
+                s = 0;
+                ++u;
+            }
+            if (++e == kPF) e = 0;
+            pos_next(a, NG, nchunks, total, cur);
+        }
+        tc::cp_async_wait<0>();
     } else if (warp == kMmaWarp) {
         // ================= MMA issuer =================
-        uint32_t gc = 0, tcnt = 0, ic = 0;
+        uint32_t gc = 0, tcnt = 0, ic = 0, u = 0;
+        int s = 0;
+        const uint64_t bdesc0 = tc::smem_desc_sw128(tc::smem_u32(Bres));
         for (int64_t item = blockIdx.x; item < total; item += gridDim.x, ++ic) {
             const Item it = decode_item(a, NG, item);
             const uint32_t idesc = tc::idesc_i8(kTM, it.ncols16, /*a_signed=*/true);
-            const uint32_t baddr = tc::smem_u32(Bres);
             for (int t = 0; t < it.ntiles; ++t, ++tcnt) {
                 const int b = tcnt & 1;
                 const uint32_t ub = tcnt >> 1;
@@ -275,31 +309,30 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                 if (ub > 0) tc::mbar_wait(&acce_bar[b], (ub - 1) & 1);
                 if (lane == 0) RQ_TR(12, tcnt);
                 tc::fence_after_sync();
-                const uint32_t dacc = tmem + (uint32_t)(b * kTN);
+                const uint32_t dacc = tmem + (uint32_t)b * sp.acc_cols;
                 for (int c = 0; c < nchunks; ++c, ++gc) {
-                    const int s = gc % nst;
-                    const uint32_t u = gc / nst;
-                    const int kbytes = min(kKC, a.Dp - c * kKC);
+                    const int nks = min(kKC, a.Dp - c * kKC) / 32;
                     if (lane == 0) RQ_TR(7, gc);
                     if (t == 0) tc::mbar_wait(&bfull_bar[c], ic & 1);
-                    if (lane == 0) RQ_TR(8, gc);
                     tc::mbar_wait(&full_bar[s], u & 1);
                     tc::fence_after_sync();
                     if (lane == 0) RQ_TR(9, gc);
-                    if (lane == 0) {
-                        const uint32_t aaddr = tc::smem_u32(stA + s * kStageA);
-                        const int nks = (a.experiment & 2) ? ((c == 0) ? 1 : 0) : kbytes / 32;
-                        for (int ks = 0; ks < nks; ++ks) {
-                            const uint64_t ad = tc::smem_desc(aaddr + ks * 256, 128, kSBO);
-                            const uint64_t bd = tc::smem_desc_sw128(baddr + c * bchunk + ks * 32);
-                            tc::mma_i8(dacc, ad, bd, idesc, (c > 0 || ks > 0) ? 1u : 0u);
-                        }
-                        tc::commit(&empty_bar[s]);                          // A stage s free once these retire
-                        if (t == it.ntiles - 1) tc::commit(&bfree_bar[c]);  // B chunk c free for the next item
-                        if (c == nchunks - 1) tc::commit(&accf_bar[b]);     // accumulator b complete
-                        RQ_TR(10, gc);
+                    {
+                        const uint32_t aaddr = tmemA + (uint32_t)(s * kChunkCols);
+                        const uint64_t bd = bdesc0 + (uint64_t)((c * bchunk) >> 4);
+                        const int n = (a.experiment & 2) ? ((c == 0) ? 1 : 0) : nks;
+                        for (int ks = 0; ks < n; ++ks)
+                            tc::mma_i8_ts_warp(dacc, aaddr + 8 * ks, bd + (uint64_t)(ks * 2), idesc,
+                                               (c > 0 || ks > 0) ? 1u : 0u);
+                        tc::commit_warp(&empty_bar[s]);                          // A slot s free once these retire
+                        if (t == it.ntiles - 1) tc::commit_warp(&bfree_bar[c]);  // B chunk c free for the next item
+                        if (c == nchunks - 1) tc::commit_warp(&accf_bar[b]);     // accumulator b complete
+                        if (lane == 0) RQ_TR(10, gc);
                     }
-                    __syncwarp();
+                    if (++s == nsl) {
+                        s = 0;
+                        ++u;
+                    }
                 }
             }
         }
@@ -372,20 +405,16 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
 #pragma unroll 1
                 for (int hc = half; hc * 32 < ((a.experiment & 1) ? 0 : it.ncols); hc += 2) {
                     const int col0 = hc * 32;
+                    const uint32_t tcol = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)b * sp.acc_cols + col0;
                     uint32_t acc[32];
-                    tc::tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * kTN + col0), acc);
-                    // phase 1: keys + survivor ballots of 32 columns; lane i keeps column i's ballot
-                    float key[32];
-                    uint32_t myballot = 0u;
+                    tc::tmem_ld32(tcol, acc);
+                    // phase 1: bit i of rowbits = this row survives against column i
+                    uint32_t rowbits = 0u;
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
                         const ColC& cc = cb[col0 + i];  // empty columns have tau = -inf
-                        // acc = -ip (s8 codes in {0, -1}); 0x4B400000 + n is the float
-                        // 1.5 2^23 + n exactly for |n| < 2^22, so ipn = -ip exactly
-                        const float ipn = __fsub_rn(__int_as_float(0x4B400000 + (int)acc[i]), 12582912.0f);
-                        const float tt = __fmaf_rn(-cc.c.a, ipn, __fmaf_rn(cc.c.b, pcf, -cc.c.K));
-                        const float est = __fmaf_rn(-fac.y, tt, __fadd_rn(fac.x, cc.c.nq2));
-                        key[i] = rank_key<kLB>(est, cc.epsnq, g1);
+                        const float est = est_of(acc[i], cc, fac, pcf);
+                        const float key = rank_key<kLB>(est, cc.epsnq, g1);
                         if constexpr (kDump) {
                             if (vok && col0 + i < it.ncols) {
                                 const int64_t di = (a.item_off[cc.pair] + (v >> 5)) * 32 + (v & 31);
@@ -397,27 +426,38 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                         }
                         bool sv;
                         if constexpr (kRetry) {  // exact (key, row) <= tau64 (overflow / underflow re-scan)
-                            const uint32_t ko = f2o(key[i]), to = f2o(cc.tau);
-                            sv = vok && (ko < to || (ko == to && row <= (uint32_t)cc.pair));
+                            const uint32_t ko = f2o(key), to = f2o(cc.tau);
+                            sv = ko < to || (ko == to && row <= (uint32_t)cc.pair);
                         } else {
-                            sv = vok && key[i] <= cc.tau;
+                            sv = key <= cc.tau;
                         }
-                        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, sv);
-                        if (lane == i) myballot = bal;
+                        rowbits |= sv ? (1u << i) : 0u;
                     }
-                    // phase 2: one atomic per surviving column, all issued together by their lanes
-                    const uint32_t cols = __ballot_sync(0xFFFFFFFFu, myballot != 0u);
+                    if (!vok) rowbits = 0u;
+                    uint32_t cols = __reduce_or_sync(0xFFFFFFFFu, rowbits);
                     if (cols) {
+                        // phase 2 (surviving columns only): lane i takes column i's ballot,
+                        // then one atomic per column, all issued together
+                        uint32_t mybal = 0u;
+                        for (uint32_t m = cols; m; m &= m - 1) {
+                            const int i = __ffs(m) - 1;
+                            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, (rowbits >> i) & 1u);
+                            if (lane == i) mybal = bal;
+                        }
                         int mybase = 0;
-                        if (myballot) mybase = atomicAdd(&a.cnt[cb[col0 + lane].q], __popc(myballot));
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) {
-                            if (!(cols >> i & 1u)) continue;  // warp-uniform
-                            const uint32_t bal = __shfl_sync(0xFFFFFFFFu, myballot, i);
+                        if (mybal) mybase = atomicAdd(&a.cnt[cb[col0 + lane].q], __popc(mybal));
+                        // phase 3: survivors re-read their accumulator column and store
+                        // (key, row); same arithmetic as phase 1, same key
+                        for (uint32_t m = cols; m; m &= m - 1) {
+                            const int i = __ffs(m) - 1;
+                            const uint32_t bal = __shfl_sync(0xFFFFFFFFu, mybal, i);
                             const int base = __shfl_sync(0xFFFFFFFFu, mybase, i);
-                            if (bal >> lane & 1u) {
+                            const uint32_t acci = tc::tmem_ld1(tcol + (uint32_t)i);
+                            if ((bal >> lane) & 1u) {
+                                const ColC& cc = cb[col0 + i];
+                                const float key = rank_key<kLB>(est_of(acci, cc, fac, pcf), cc.epsnq, g1);
                                 const int pos = base + __popc(bal & ((1u << lane) - 1u));
-                                if (pos < a.cap) a.buf[(size_t)cb[col0 + i].q * a.cap + pos] = make_key(key[i], row);
+                                if (pos < a.cap) a.buf[(size_t)cc.q * a.cap + pos] = make_key(key, row);
                             }
                         }
                     }
@@ -523,7 +563,7 @@ __global__ void list_items_kernel(int nlist, const int64_t* __restrict__ list_of
 
 bool imma_wanted(const rabitq_index* idx, int64_t npairs, int scan_path) {
     if (scan_path == RABITQ_SCAN_POPC) return false;
-    if (idx->W > 2 * kWPT || idx->W > 4 * kMaxChunks) return false;  // producer registers / B chunks (D <= 1024)
+    if (idx->W > 4 * kMaxChunks) return false;  // B chunks (D <= 1024)
     if (scan_path == RABITQ_SCAN_IMMA) return true;
     // AUTO: the tensor-core path pays once lists are shared by enough queries
     return npairs >= (int64_t)8 * idx->nlist;
@@ -621,7 +661,8 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     RQ_REQUIRE(cr == CUDA_SUCCESS, RABITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
     const SmemPlan plan = smem_plan(a.Dp);
-    RQ_REQUIRE(plan.stages >= 2, RABITQ_ERR_INTERNAL, "grouped scan: shared-memory plan has < 2 stages");
+    RQ_REQUIRE(plan.slots >= 2 && plan.total <= (uint32_t)kSmemLimit, RABITQ_ERR_INTERNAL,
+               "grouped scan: TMEM / shared-memory plan does not fit");
     const size_t smem = plan.total;
     const int grid = sms;
 #define RQ_IMMA(LB, DP, RT)                                                                                     \
