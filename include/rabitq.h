@@ -191,6 +191,16 @@ void rabitq_free(rabitq_index* idx); /* NULL is a no-op */
 const char* rabitq_last_error(void);
 const char* rabitq_version(void);
 
+/* Device self-check of an arithmetic identity the search path relies on
+ * (diagnostics; no index needed).  what = 1: the quantizer's reciprocal
+ * division (search.cu div_rcp_rn, R#11: t = fl(x / Delta) must equal the IEEE
+ * quotient) against __fdiv_rn on n seeded random (x, Delta) pairs drawn from
+ * the quantizer's domain (Delta > 0 normal, 0 <= x / Delta <= 15.01) plus
+ * arbitrary bit patterns with quotients in range.  *mismatches (host) receives
+ * the number of differing quotients.  Runs on the current CUDA device.
+ * Errors: what unknown or mismatches NULL -> INVALID_ARGUMENT. */
+rabitq_status rabitq_selftest(int32_t what, uint64_t n, uint64_t seed, uint64_t* mismatches);
+
 /* ------------------------------------------ multi-GPU -- */
 /* One process per GPU.  Rank 0 calls rabitq_comm_unique_id, the id travels
  * through the caller's process group (e.g. torch.distributed), every rank

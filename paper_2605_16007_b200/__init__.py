@@ -120,7 +120,7 @@ EXPORTED = [
     "rabitq_build", "rabitq_build_ex", "rabitq_build_opts_default", "rabitq_search", "rabitq_search_ex",
     "rabitq_search_opts_default", "rabitq_index_info", "rabitq_index_export", "rabitq_free",
     "rabitq_last_error", "rabitq_version", "rabitq_comm_unique_id", "rabitq_comm_init", "rabitq_comm_free",
-    "rabitq_search_sharded", "rabitq_merge_topk",
+    "rabitq_search_sharded", "rabitq_merge_topk", "rabitq_selftest",
 ]
 
 _lib = None
@@ -332,3 +332,11 @@ class Comm:
 
 def version() -> str:
     return lib().rabitq_version().decode()
+
+
+def selftest(what: int, n: int, seed: int = 0) -> int:
+    """rabitq_selftest: number of mismatches of a device arithmetic identity
+    (what = 1: the quantizer's reciprocal division vs IEEE division)."""
+    out = ctypes.c_uint64(0)
+    _check(lib().rabitq_selftest(ctypes.c_int32(what), ctypes.c_uint64(n), ctypes.c_uint64(seed), ctypes.byref(out)))
+    return int(out.value)

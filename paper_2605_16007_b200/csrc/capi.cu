@@ -156,6 +156,22 @@ struct rabitq_comm {
 extern "C" {
 
 const char* rabitq_last_error(void) { return g_err.c_str(); }
+rabitq_status rabitq_selftest(int32_t what, uint64_t n, uint64_t seed, uint64_t* mismatches) {
+    API_BEGIN
+    RQ_REQUIRE(mismatches != nullptr, RABITQ_ERR_INVALID_ARGUMENT, "mismatches is NULL");
+    RQ_REQUIRE(what == 1, RABITQ_ERR_INVALID_ARGUMENT, "unknown selftest");
+    cudaStream_t st = nullptr;
+    RQ_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    try {
+        *mismatches = rabitq::selftest_div(n, seed, st);
+    } catch (...) {
+        cudaStreamDestroy(st);
+        throw;
+    }
+    RQ_CUDA(cudaStreamDestroy(st));
+    API_END
+}
+
 const char* rabitq_version(void) { return "librabitq 0.1 (IVF-RaBitQ search hot path, sm_100a)"; }
 
 void rabitq_build_opts_default(rabitq_build_opts* o) {

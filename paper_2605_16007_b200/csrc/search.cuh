@@ -142,6 +142,7 @@ void search_batch(const rabitq_index* idx, const float* Q, int64_t nq, int k, in
                   const SearchCfg& cfg, int64_t qid_base, int64_t* ids, float* dists, const DebugOut& dbg,
                   cudaStream_t st, SearchStats* stats);
 void scan_imma(const ScanArgs& a, bool lb, bool dump, bool retry, cudaStream_t st);
+uint64_t selftest_div(uint64_t n, uint64_t seed, cudaStream_t st);
 void scan_popc_entry(const ScanArgs& a, bool lb, bool retry, bool dump, cudaStream_t st);
 void merge_topk(const int64_t* in_ids, const float* in_d, int G, int64_t nq, int k, int64_t* out_ids,
                 float* out_d, cudaStream_t st);

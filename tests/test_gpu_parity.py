@@ -336,3 +336,13 @@ def test_borrow_and_shard_offsets(orc):
     assert ids.min() >= lo and ids.max() < hi
     gi, gd = orc.bruteforce(X.numpy()[lo:hi], Q.numpy(), 10)
     pu.check_final(ids, d.cpu().numpy(), gi + lo, gd.astype(np.float32), 10)
+
+
+def test_selftest_reciprocal_division():
+    """The quantizer divides with a per-pair reciprocal (Markstein correction);
+    R#11 pins t = fl((r - v_l) / Delta) to the IEEE quotient, so the two must be
+    bit-identical on the quantizer's domain and on arbitrary normal operands."""
+    assert rq.selftest(1, 1 << 28, seed=7) == 0
+    assert rq.selftest(1, 1 << 26, seed=12345) == 0
+    with pytest.raises(rq.RabitqError):
+        rq.selftest(99, 1)

@@ -17,6 +17,7 @@ ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--nq", type=int, default=0)
 ap.add_argument("--runs", default='[{}]', help="JSON list of search kwargs")
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--profile-last", action="store_true", help="cudaProfilerStart/Stop around the last rep (ncu --profile-from-start off)")
 args = ap.parse_args()
 s = synth.spec(args.config, **({"nq": args.nq} if args.nq else {}))
 dev = torch.device("cuda", 0)
@@ -30,12 +31,18 @@ print("build_s", round(time.time() - t0, 2), idx.info(), flush=True)
 st = torch.cuda.Stream(dev)
 for kw in json.loads(args.runs):
     for rep in range(args.reps):
+        last = args.profile_last and rep == args.reps - 1
+        if last:
+            torch.cuda.synchronize()
+            torch.cuda.cudart().cudaProfilerStart()
         prof = rq.Profile()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
         ids, d = idx.search(Q, s.k, kw.pop("nprobe", s.nprobe) if False else s.nprobe, s.M, stream=st, profile=prof, **kw)
         e1.record(st)
         torch.cuda.synchronize()
+        if last:
+            torch.cuda.cudart().cudaProfilerStop()
         pd = prof.as_dict()
         pd["stage_ms"] = {k: round(v, 3) for k, v in pd["stage_ms"].items()}
         print(json.dumps({"kw": kw, "rep": rep, "ms": round(e0.elapsed_time(e1), 3), **pd}), flush=True)
