@@ -192,7 +192,7 @@ __device__ __forceinline__ void pos_next(const ScanArgs& a, int NG, int nchunks,
 //              item), chunk c of the next item as soon as chunk c is free
 //   warps 6-13 epilogue: tcgen05.ld the int32 inner products, fused
 //              estimator (+ bound), threshold, survivor append
-template <bool kLB, bool kDump, bool kRetry>
+template <bool kLB, bool kDump, bool kRetry, bool kDense>
 __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant__ CUtensorMap tmapB, ScanArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
@@ -265,7 +265,7 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
             tc::cp_async_wait<kPF - 1>();  // this thread's words of chunk gc have landed
             const uint4 wv = *reinterpret_cast<const uint4*>(raw + (e * kTM + r) * 4);
             if (tid == 0) RQ_TR(0, gc);
-            if (u > 0) tc::mbar_wait(&empty_bar[s], (u - 1) & 1);
+            if (u > 0) tc::mbar_wait_backoff(&empty_bar[s], (u - 1) & 1);
             tc::fence_after_sync();
             if (tid == 0) RQ_TR(1, gc);
             const uint32_t dst = tmemA + (uint32_t)(s * kChunkCols) + lane_addr;
@@ -306,7 +306,7 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                 const int b = tcnt & 1;
                 const uint32_t ub = tcnt >> 1;
                 if (lane == 0) RQ_TR(11, tcnt);
-                if (ub > 0) tc::mbar_wait(&acce_bar[b], (ub - 1) & 1);
+                if (ub > 0) tc::mbar_wait_backoff(&acce_bar[b], (ub - 1) & 1);
                 if (lane == 0) RQ_TR(12, tcnt);
                 tc::fence_after_sync();
                 const uint32_t dacc = tmem + (uint32_t)b * sp.acc_cols;
@@ -343,7 +343,7 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
             for (int64_t item = blockIdx.x; item < total; item += gridDim.x, ++ic) {
                 const Item it = decode_item(a, NG, item);
                 for (int c = 0; c < nchunks; ++c) {
-                    if (ic > 0) tc::mbar_wait(&bfree_bar[c], (ic - 1) & 1);  // previous item done with chunk c
+                    if (ic > 0) tc::mbar_wait_backoff(&bfree_bar[c], (ic - 1) & 1);  // previous item done with chunk c
                     tc::mbar_arrive_expect_tx(&bfull_bar[c], (uint32_t)(it.nboxes * kBoxRows * kKC));
                     for (int bx = 0; bx < it.nboxes; ++bx)
                         tc::tma_load_2d(Bres + c * bchunk + bx * kBoxRows * kKC, &tmapB, &bfull_bar[c], c * kKC,
@@ -408,6 +408,18 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                     const uint32_t tcol = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)b * sp.acc_cols + col0;
                     uint32_t acc[32];
                     tc::tmem_ld32(tcol, acc);
+                    if constexpr (kDense) {
+                        // sample scan: every key, coalesced (lanes = consecutive vectors);
+                        // the column's absolute offset rides in (q, pair)
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            const ColC& cc = cb[col0 + i];
+                            const float key = rank_key<kLB>(est_of(acc[i], cc, fac, pcf), cc.epsnq, g1);
+                            const int64_t off = ((int64_t)(uint32_t)cc.pair << 32) | (uint32_t)cc.q;
+                            if (vok && col0 + i < it.ncols) a.dense_keys[off + v] = f2o(key);
+                        }
+                        continue;
+                    }
                     // phase 1: bit i of rowbits = this row survives against column i
                     uint32_t rowbits = 0u;
 #pragma unroll
@@ -526,7 +538,8 @@ __global__ void compact_flagged_kernel(const int* __restrict__ flags, int max_ra
 // (re-scan: tau / pair carry the 64-bit (key, row) threshold instead)
 __global__ void colc_kernel(const int32_t* __restrict__ gpair, int64_t npairs, int nprobe, int D,
                             const float4* __restrict__ qscal, const float* __restrict__ tau,
-                            const uint64_t* __restrict__ tau64, float eps0, ColC* __restrict__ gcolc) {
+                            const uint64_t* __restrict__ tau64, float eps0, const int64_t* __restrict__ dbase,
+                            const int64_t* __restrict__ doff, ColC* __restrict__ gcolc) {
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < npairs; g += (int64_t)gridDim.x * blockDim.x) {
         const int p = gpair[g];
         const int q = p / nprobe;
@@ -534,7 +547,12 @@ __global__ void colc_kernel(const int32_t* __restrict__ gpair, int64_t npairs, i
         cc.c = pair_consts(qscal[p], D);
         cc.epsnq = __fmul_rn(eps0, sqrtf(cc.c.nq2));
         cc.q = q;
-        if (tau64) {
+        if (dbase) {  // dense key dump: absolute offset of the pair's keys in (q, pair)
+            const int64_t off = dbase[q] + doff[p];
+            cc.tau = INFINITY;
+            cc.q = (int)(uint32_t)off;
+            cc.pair = (int)(uint32_t)(off >> 32);
+        } else if (tau64) {
             cc.tau = o2f((uint32_t)(tau64[q] >> 32));
             cc.pair = (int)(uint32_t)tau64[q];
         } else {
@@ -604,6 +622,21 @@ void prepare_groups(const rabitq_index* idx, const int32_t* probes, int64_t n, c
     launches += 7;
 }
 
+void group_items(const rabitq_index* idx, const int64_t* list_off, const Groups& g, WBuf<int64_t>& itemc,
+                 WBuf<int64_t>& items, cudaStream_t st, int& launches) {
+    const int nlist = idx->nlist;
+    itemc.alloc((size_t)nlist + 1, st);
+    items.alloc((size_t)nlist + 1, st);
+    list_items_kernel<<<(nlist + 256) / 256, 256, 0, st>>>(nlist, list_off, g.gcount.p, group_cols(g.Dp), itemc.p);
+    RQ_CHECK_LAUNCH();
+    size_t tb = 0;
+    RQ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, itemc.p, items.p, nlist + 1, st));
+    WBuf<uint8_t> tmp;
+    tmp.alloc(tb, st);
+    RQ_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, itemc.p, items.p, nlist + 1, st));
+    launches += 3;
+}
+
 int64_t regroup_flagged(const rabitq_index* idx, const int32_t* probes, int64_t npairs, int nprobe, const int* flags,
                         int max_rank, const Groups& full, Groups& sub, cudaStream_t st, int& launches) {
     WBuf<int32_t> list;
@@ -639,12 +672,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_t st) {
+void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_t st, bool dense) {
     ScanArgs a = a_in;  // a.npairs = grouped rows (all pairs, or the re-scan's sub list)
     WBuf<ColC> gcolc;
     gcolc.alloc((size_t)a.npairs + kTN, st);
     colc_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((a.npairs + 255) / 256, 2048)), 256, 0, st>>>(
-        a.gpair, a.npairs, a.nprobe, a.D, a.qscal, a.tau, retry ? a.tau64 : nullptr, a.eps0, gcolc.p);
+        a.gpair, a.npairs, a.nprobe, a.D, a.qscal, a.tau, retry ? a.tau64 : nullptr, a.eps0,
+        dense ? a.dense_base : nullptr, dense ? a.dense_off : nullptr, gcolc.p);
     RQ_CHECK_LAUNCH();
     a.gcolc = gcolc.p;
     int dev = 0, sms = 148;
@@ -665,13 +699,17 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
                "grouped scan: TMEM / shared-memory plan does not fit");
     const size_t smem = plan.total;
     const int grid = sms;
-#define RQ_IMMA(LB, DP, RT)                                                                                     \
+#define RQ_IMMA4(LB, DP, RT, DN)                                                                               \
     do {                                                                                                        \
-        RQ_CUDA(cudaFuncSetAttribute(scan_imma_kernel<LB, DP, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                     (int)smem));                                                               \
-        scan_imma_kernel<LB, DP, RT><<<grid, kNT, smem, st>>>(tmap, a);                                         \
+        RQ_CUDA(cudaFuncSetAttribute(scan_imma_kernel<LB, DP, RT, DN>,                                          \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));                  \
+        scan_imma_kernel<LB, DP, RT, DN><<<grid, kNT, smem, st>>>(tmap, a);                                     \
     } while (0)
-    if (dump) {
+#define RQ_IMMA(LB, DP, RT) RQ_IMMA4(LB, DP, RT, false)
+    if (dense) {
+        if (lb) RQ_IMMA4(true, false, false, true);
+        else RQ_IMMA4(false, false, false, true);
+    } else if (dump) {
         if (lb) RQ_IMMA(true, true, false);
         else RQ_IMMA(false, true, false);
     } else if (retry) {
@@ -682,6 +720,7 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
         else RQ_IMMA(false, false, false);
     }
 #undef RQ_IMMA
+#undef RQ_IMMA4
     RQ_CHECK_LAUNCH();
 }
 

@@ -49,6 +49,11 @@ struct ScanArgs {
     int experiment;            // diagnostics (RABITQ_IMMA_EXPERIMENT): 1 skip epilogue math, 2 skip UMMAs
     long long* trace;          // diagnostics (RABITQ_SCAN_TRACE): clock64 stamps of CTA 0, [trace_n][16]
     int trace_n;
+    // dense key dump (threshold-seeding sample scan): key of every scanned pair
+    // at dense_keys[dense_base[q] + dense_off[pair] + v]
+    uint32_t* dense_keys;
+    const int64_t* dense_base;  // [nq] first key of each query
+    const int64_t* dense_off;   // [npairs] offset of each (query, probe) pair within its query
 };
 
 template <typename T>
@@ -141,7 +146,10 @@ struct SearchStats {
 void search_batch(const rabitq_index* idx, const float* Q, int64_t nq, int k, int nprobe, int M,
                   const SearchCfg& cfg, int64_t qid_base, int64_t* ids, float* dists, const DebugOut& dbg,
                   cudaStream_t st, SearchStats* stats);
-void scan_imma(const ScanArgs& a, bool lb, bool dump, bool retry, cudaStream_t st);
+void scan_imma(const ScanArgs& a, bool lb, bool dump, bool retry, cudaStream_t st, bool dense = false);
+// list_items of a grouping for other list sizes (sample-scan view)
+void group_items(const rabitq_index* idx, const int64_t* list_off, const Groups& g, WBuf<int64_t>& itemc,
+                 WBuf<int64_t>& items, cudaStream_t st, int& launches);
 uint64_t selftest_div(uint64_t n, uint64_t seed, cudaStream_t st);
 void scan_popc_entry(const ScanArgs& a, bool lb, bool retry, bool dump, cudaStream_t st);
 void merge_topk(const int64_t* in_ids, const float* in_d, int G, int64_t nq, int k, int64_t* out_ids,
