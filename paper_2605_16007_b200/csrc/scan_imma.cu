@@ -52,8 +52,9 @@ constexpr int kProdWarps = 4;              // thread r expands code row r into T
 constexpr int kMmaWarp = kProdWarps;       // warp 4 issues the UMMAs (and owns TMEM)
 constexpr int kLoadWarp = kProdWarps + 1;  // warp 5 streams the query operand (TMA)
 constexpr int kEpiWarp0 = kProdWarps + 2;  // warps 6..13
-constexpr int kEpiWarps = 8;
-constexpr int kNT = (kEpiWarp0 + kEpiWarps) * 32;  // 448 threads: <= 4 warps per SMSP -> 128 registers
+constexpr int kEpiWarps = 16;              // 4 per TMEM lane quarter, columns interleaved in chunks of kEC
+constexpr int kEC = 16;                    // accumulator columns per epilogue step
+constexpr int kNT = (kEpiWarp0 + kEpiWarps) * 32;  // 704 threads (80 registers)
 constexpr int kTmemCols = 512;
 constexpr int kPF = 8;                     // code-word prefetch ring (chunks in flight per producer thread)
 constexpr int kSmemLimit = 227 * 1024;
@@ -355,14 +356,14 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
         // ================= epilogue =================
         const int e = warp - kEpiWarp0;     // 0..7
         const int quarter = warp & 3;       // TMEM lanes this warp may access: 32 * (warp % 4) ..
-        const int half = e >> 2;            // interleaved 32-column chunks: half, half + 2, ...
+        const int part = e >> 2;            // interleaved kEC-column chunks: part, part + kEpiWarps / 4, ...
         const int r = quarter * 32 + lane;  // tile row = vector
-        const int et = e * 32 + lane;       // 0..255 among epilogue threads
+        const int et = e * 32 + lane;       // index among the epilogue threads (>= NG)
         uint32_t ic = 0, tcnt = 0;
         int64_t item = blockIdx.x;
         Item it{};
         ColC nextc;
-        auto fetch_colc = [&](const Item& x) {  // one coalesced 32-byte load per column (NG <= 256)
+        auto fetch_colc = [&](const Item& x) {  // one coalesced 32-byte load per column (NG <= 32 kEpiWarps)
             if (et < x.ncols) {
                 nextc = a.gcolc[x.grow0 + et];
             } else {
@@ -403,16 +404,16 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                 if (e == 0 && lane == 0) RQ_TR(14, tcnt);
                 tc::fence_after_sync();
 #pragma unroll 1
-                for (int hc = half; hc * 32 < ((a.experiment & 1) ? 0 : it.ncols); hc += 2) {
-                    const int col0 = hc * 32;
+                for (int hc = part; hc * kEC < ((a.experiment & 1) ? 0 : it.ncols); hc += kEpiWarps / 4) {
+                    const int col0 = hc * kEC;
                     const uint32_t tcol = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)b * sp.acc_cols + col0;
-                    uint32_t acc[32];
-                    tc::tmem_ld32(tcol, acc);
+                    uint32_t acc[kEC];
+                    tc::tmem_ld16(tcol, acc);
                     if constexpr (kDense) {
                         // sample scan: every key, coalesced (lanes = consecutive vectors);
                         // the column's absolute offset rides in (q, pair)
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) {
+                        for (int i = 0; i < kEC; ++i) {
                             const ColC& cc = cb[col0 + i];
                             const float key = rank_key<kLB>(est_of(acc[i], cc, fac, pcf), cc.epsnq, g1);
                             const int64_t off = ((int64_t)(uint32_t)cc.pair << 32) | (uint32_t)cc.q;
@@ -423,7 +424,7 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                     // phase 1: bit i of rowbits = this row survives against column i
                     uint32_t rowbits = 0u;
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
+                    for (int i = 0; i < kEC; ++i) {
                         const ColC& cc = cb[col0 + i];  // empty columns have tau = -inf
                         const float est = est_of(acc[i], cc, fac, pcf);
                         const float key = rank_key<kLB>(est, cc.epsnq, g1);
@@ -457,7 +458,7 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                             if (lane == i) mybal = bal;
                         }
                         int mybase = 0;
-                        if (mybal) mybase = atomicAdd(&a.cnt[cb[col0 + lane].q], __popc(mybal));
+                        if (mybal) mybase = atomicAdd(&a.cnt[cb[col0 + (lane & (kEC - 1))].q], __popc(mybal));
                         // phase 3: survivors re-read their accumulator column and store
                         // (key, row); same arithmetic as phase 1, same key
                         for (uint32_t m = cols; m; m &= m - 1) {
