@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "index.cuh"
@@ -31,6 +32,40 @@ __global__ void gather_rows_kernel(const float* __restrict__ X, int D, const int
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = e / D, d = e % D;
         out[e] = X[(size_t)rows[i] * D + d];
+    }
+}
+
+// slot-ordered copy of the fp32 vectors, centred on their list's centroid in
+// the original space (x - c_j; pad slots zero): a list's rows are contiguous
+// for TMA, and the dense re-rank's GEMM form ||q-c||^2 + ||x-c||^2 - 2 (q-c).(x-c)
+// works on residuals instead of raw vectors (no cancellation of large norms)
+__global__ void slot_rows_kernel(const float* __restrict__ X, int D, const uint32_t* __restrict__ rows,
+                                 const int64_t* __restrict__ slot_off, const float* __restrict__ Corig, int nlist,
+                                 float* __restrict__ Xs) {
+    const int per = D / 4;
+    for (int j = blockIdx.x; j < nlist; j += gridDim.x) {
+        const int64_t s0 = slot_off[j], s1 = slot_off[j + 1];
+        const float4* c = reinterpret_cast<const float4*>(Corig + (size_t)j * D);
+        for (int64_t e = threadIdx.x; e < (s1 - s0) * per; e += blockDim.x) {
+            const int64_t s = s0 + e / per;
+            const int k = (int)(e % per);
+            const uint32_t r = rows[s];
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (r != kPadRow) {
+                const float4 x = reinterpret_cast<const float4*>(X + (size_t)r * D)[k];
+                const float4 cc = c[k];
+                v = make_float4(__fsub_rn(x.x, cc.x), __fsub_rn(x.y, cc.y), __fsub_rn(x.z, cc.z), __fsub_rn(x.w, cc.w));
+            }
+            reinterpret_cast<float4*>(Xs + (size_t)s * D)[k] = v;
+        }
+    }
+}
+
+// Pt = P^T (the rotation's B operand for the tensor-core GEMM: rows of P^T are K-contiguous)
+__global__ void transpose_kernel(const float* __restrict__ P, int D, float* __restrict__ Pt) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)D * D; e += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(e / D), j = (int)(e % D);
+        Pt[(int64_t)j * D + i] = P[e];
     }
 }
 
@@ -227,6 +262,8 @@ std::vector<int64_t> stratified(int64_t n, int64_t m, uint64_t seed, uint32_t ta
 
 void free_index_memory(rabitq_index* idx) {
     cudaFree(idx->P);
+    cudaFree(idx->Pt);
+    idx->Pt = nullptr;
     cudaFree(idx->Cr);
     cudaFree(idx->cnorm);
     cudaFree(idx->list_off);
@@ -241,6 +278,10 @@ void free_index_memory(rabitq_index* idx) {
     cudaFree(idx->rows);
     cudaFree(idx->slot_of_row);
     cudaFree(idx->X_owned);
+    cudaFree(idx->Xs);
+    idx->Xs = nullptr;
+    cudaFree(idx->Corig);
+    idx->Corig = nullptr;
     idx->P = idx->Cr = idx->cnorm = nullptr;
     idx->list_off = idx->slot_off = nullptr;
     idx->codes = nullptr;
@@ -301,6 +342,9 @@ void build_index(rabitq_index* idx, const float* X, int64_t n, int D, int nlist,
         RQ_CUDA(cudaMemcpyAsync(idx->P, hP.data(), hP.size() * sizeof(float), cudaMemcpyHostToDevice, st));
         RQ_CUDA(cudaStreamSynchronize(st));
     }
+    RQ_CUDA(cudaMalloc(&idx->Pt, (size_t)D * D * sizeof(float)));
+    transpose_kernel<<<grid_for((int64_t)D * D), 256, 0, st>>>(idx->P, D, idx->Pt);
+    RQ_CHECK_LAUNCH();
     RQ_CUDA(cudaMalloc(&idx->Cr, (size_t)nlist * D * sizeof(float)));
     RQ_CUDA(cudaMalloc(&idx->cnorm, (size_t)nlist * sizeof(float)));
 
@@ -476,6 +520,25 @@ void build_index(rabitq_index* idx, const float* X, int64_t n, int D, int nlist,
                                                     idx->n_o, idx->rho, idx->rows, idx->slot_of_row, idx->pcnt);
         RQ_CHECK_LAUNCH();
         RQ_CUDA(cudaStreamSynchronize(st));
+    }
+
+    // ---- slot-ordered vectors for the dense re-rank (when they fit comfortably) ----
+    {
+        const char* env = getenv("RABITQ_SLOT_VECTORS");  // "0": never build the copy
+        size_t freeb = 0, totalb = 0;
+        RQ_CUDA(cudaMemGetInfo(&freeb, &totalb));
+        const size_t bytes = (size_t)(idx->nslots + 128) * D * sizeof(float);
+        if (D % 4 == 0 && !(env && env[0] == '0') && bytes <= (size_t)(0.4 * (double)freeb)) {
+            // original-space centroids c = P c' (row form: C = C' P^T)
+            RQ_CUDA(cudaMalloc(&idx->Corig, (size_t)nlist * D * sizeof(float)));
+            sgemm(nlist, D, D, idx->Cr, D, idx->Pt, D, false, idx->Corig, D, 0, nullptr, st);
+            RQ_CUDA(cudaMalloc(&idx->Xs, bytes));
+            RQ_CUDA(cudaMemsetAsync(idx->Xs + (size_t)idx->nslots * D, 0, (size_t)128 * D * sizeof(float), st));
+            slot_rows_kernel<<<std::min(nlist, 4096), 256, 0, st>>>(idx->X, D, idx->rows, idx->slot_off, idx->Corig,
+                                                                    nlist, idx->Xs);
+            RQ_CHECK_LAUNCH();
+            RQ_CUDA(cudaStreamSynchronize(st));
+        }
     }
 }
 

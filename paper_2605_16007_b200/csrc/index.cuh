@@ -20,6 +20,7 @@ struct rabitq_index {
     uint64_t seed = 0;
 
     float* P = nullptr;            // [D x D] row-major, x' = P^T x
+    float* Pt = nullptr;           // [D x D] P^T row-major (tensor-core rotation operand)
     float* Cr = nullptr;           // [nlist x D] rotated centroids c'
     float* cnorm = nullptr;        // [nlist] ||c'||^2
     int64_t* list_off = nullptr;   // [nlist + 1] list boundaries in list order (rank of vector)
@@ -33,6 +34,10 @@ struct rabitq_index {
     uint32_t* rows = nullptr;      // [nslots] local row id, kPadRow for pad slots
     uint32_t* slot_of_row = nullptr;  // [n] inverse of rows (debug capture of bounds)
     const float* X = nullptr;      // [n x D] fp32 vectors for the exact re-rank (local rows)
+    float* Xs = nullptr;           // [nslots + 128 x D] the same vectors in slot (list) order, minus their
+                                   // list centroid (original space), pad slots 0; nullable (built when it
+                                   // fits; dense re-rank)
+    float* Corig = nullptr;        // [nlist x D] centroids in the original space (c = P c'), with Xs
     float* X_owned = nullptr;
     bool borrowed = false;
 

@@ -105,6 +105,12 @@ struct RerankArgs {
     const float4* qscal;
     const float* g1;
     const int32_t* order;      // [nq] block -> query (queries sharing their nearest list run together)
+    // dense re-rank of the nearest list (nullable): distance of query q to the v-th
+    // vector of its nearest list at dense_d[dpos[q] + v] (dpos[q] < 0: not covered)
+    const float* dense_d;
+    const int64_t* dpos;
+    const int64_t* list_off;
+    const float* n_o;          // [nslots] ||o - c|| (the dense distances' error scale)
 };
 
 struct SearchCfg {

@@ -39,3 +39,21 @@ for q in range(nq):
         fr[rank[int(j)]] += 1
 fr /= fr.sum()
 print(f"CFG{cfg}: share of top-M candidates by probe rank:", np.round(fr[:8], 3), "cum4", round(fr[:4].sum(), 3))
+
+# dense-tile economics: per nearest list j, queries G_j, list size L_j, candidates
+# of those queries inside j (sum) and their union
+j0 = pr[:, 0]
+sizes = np.diff(off)
+tot_c = sum(int((tid[q] >= 0).sum()) for q in range(nq))
+rows_dense, pairs_sum, pairs_union, pairs_full = 0, 0, 0, 0
+for j in np.unique(j0):
+    qs = np.where(j0 == j)[0]
+    cj = [set(tid[q][(tid[q] >= 0) & (lst[np.maximum(tid[q], 0)] == j)].tolist()) for q in qs]
+    u = set().union(*cj)
+    pairs_sum += sum(len(c) for c in cj)
+    pairs_union += len(qs) * len(u)
+    pairs_full += len(qs) * int(sizes[j])
+for thr in (1, 2, 4):
+    elig = sizes[j0] <= thr * s.M
+    print(f"  queries with nearest list <= {thr}M: {elig.mean():.3f}")
+print(f"  candidates in nearest list: {pairs_sum / tot_c:.3f}; dense pairs / needed: union {pairs_union / pairs_sum:.2f}, full list {pairs_full / pairs_sum:.2f}")
