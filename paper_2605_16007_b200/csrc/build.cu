@@ -61,6 +61,27 @@ __global__ void slot_rows_kernel(const float* __restrict__ X, int D, const uint3
     }
 }
 
+// max n_o^2 per list (the grouped scan's fast-test rounding margin)
+__global__ void list_amax_kernel(const float2* __restrict__ fac, const int64_t* __restrict__ slot_off,
+                                 const int64_t* __restrict__ list_off, int nlist, float* __restrict__ amax) {
+    __shared__ float red[8];
+    for (int j = blockIdx.x; j < nlist; j += gridDim.x) {
+        const int64_t s0 = slot_off[j], L = list_off[j + 1] - list_off[j];
+        float m = 0.0f;
+        for (int64_t v = threadIdx.x; v < L; v += blockDim.x) m = fmaxf(m, fac[s0 + v].x);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float r = 0.0f;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmaxf(r, red[w]);
+            amax[j] = r;
+        }
+        __syncthreads();
+    }
+}
+
 // Pt = P^T (the rotation's B operand for the tensor-core GEMM: rows of P^T are K-contiguous)
 __global__ void transpose_kernel(const float* __restrict__ P, int D, float* __restrict__ Pt) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)D * D; e += (int64_t)gridDim.x * blockDim.x) {
@@ -282,6 +303,8 @@ void free_index_memory(rabitq_index* idx) {
     idx->Xs = nullptr;
     cudaFree(idx->Corig);
     idx->Corig = nullptr;
+    cudaFree(idx->list_amax);
+    idx->list_amax = nullptr;
     idx->P = idx->Cr = idx->cnorm = nullptr;
     idx->list_off = idx->slot_off = nullptr;
     idx->codes = nullptr;
@@ -521,6 +544,11 @@ void build_index(rabitq_index* idx, const float* X, int64_t n, int D, int nlist,
         RQ_CHECK_LAUNCH();
         RQ_CUDA(cudaStreamSynchronize(st));
     }
+
+    RQ_CUDA(cudaMalloc(&idx->list_amax, (size_t)nlist * sizeof(float)));
+    list_amax_kernel<<<std::min(nlist, 4096), 256, 0, st>>>(idx->fac, idx->slot_off, idx->list_off, nlist,
+                                                           idx->list_amax);
+    RQ_CHECK_LAUNCH();
 
     // ---- slot-ordered vectors for the dense re-rank (when they fit comfortably) ----
     {

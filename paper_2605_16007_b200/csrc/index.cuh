@@ -28,6 +28,7 @@ struct rabitq_index {
     uint32_t* codes = nullptr;     // [nslots / 32][W][32]
     float2* fac = nullptr;         // [nslots] {n_o^2, 2 n_o / (rho sqrt(D))}
     uint16_t* pcnt = nullptr;      // [nslots] popcount of the code (grouped scan epilogue)
+    float* list_amax = nullptr;    // [nlist] max n_o^2 of each list (grouped scan fast-test margin)
     float* g1 = nullptr;           // [nslots] 2 n_o sqrt(1 - rho^2) / (rho sqrt(D - 1))  (bound / (eps0 n_q))
     float* n_o = nullptr;          // [nslots]
     float* rho = nullptr;          // [nslots]

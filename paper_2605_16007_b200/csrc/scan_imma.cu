@@ -147,9 +147,12 @@ __device__ __forceinline__ void expand32(uint32_t x, uint4& lo, uint4& hi) {
 // exactly; the rest is rabitq_est's arithmetic (a ip = (-a)(-ip) exactly).
 __device__ __forceinline__ float est_of(uint32_t acc, const ColC& cc, float2 fac, float pcf) {
     const float ipn = __fsub_rn(__int_as_float(0x4B400000 + (int)acc), 12582912.0f);
-    const float tt = __fmaf_rn(-cc.c.a, ipn, __fmaf_rn(cc.c.b, pcf, -cc.c.K));
-    return __fmaf_rn(-fac.y, tt, __fadd_rn(fac.x, cc.c.nq2));
+    const float tt = __fmaf_rn(-cc.a, ipn, __fmaf_rn(cc.b, pcf, -cc.K));
+    return __fmaf_rn(-fac.y, tt, __fadd_rn(fac.x, cc.nq2));
 }
+
+// eps0 n_q of a column (lower-bound rank key, R#15)
+#define epsnq_of(cc) __fmul_rn(a.eps0, sqrtf((cc).nq2))
 
 // clock stamps of CTA 0 (RABITQ_SCAN_TRACE diagnostics): row idx, column slot
 // (compiled in with -DRABITQ_SCAN_TRACE only; the stamps cost issue slots)
@@ -367,9 +370,9 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
             if (et < x.ncols) {
                 nextc = a.gcolc[x.grow0 + et];
             } else {
-                nextc.c = PairC{0.f, 0.f, 0.f, 0.f};
+                nextc.a = nextc.b = nextc.K = nextc.nq2 = 0.f;
                 nextc.tau = -INFINITY;
-                nextc.epsnq = 0.f;
+                nextc.U = -INFINITY;
                 nextc.q = -1;
                 nextc.pair = -1;
             }
@@ -415,34 +418,43 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
 #pragma unroll
                         for (int i = 0; i < kEC; ++i) {
                             const ColC& cc = cb[col0 + i];
-                            const float key = rank_key<kLB>(est_of(acc[i], cc, fac, pcf), cc.epsnq, g1);
+                            const float key = rank_key<kLB>(est_of(acc[i], cc, fac, pcf), epsnq_of(cc), g1);
                             const int64_t off = ((int64_t)(uint32_t)cc.pair << 32) | (uint32_t)cc.q;
                             if (vok && col0 + i < it.ncols) a.dense_keys[off + v] = f2o(key);
                         }
                         continue;
                     }
-                    // phase 1: bit i of rowbits = this row survives against column i
+                    // phase 1: bit i of rowbits = this row may survive against column i.
+                    // Main scan: fast test fma(-f, t, A) <= U (U = tau - ||r_q||^2 + a
+                    // rounding margin), a superset of est <= tau; phase 3 stores the
+                    // exact keys.  Re-scan / lower-bound key / dump: the exact key.
                     uint32_t rowbits = 0u;
 #pragma unroll
                     for (int i = 0; i < kEC; ++i) {
-                        const ColC& cc = cb[col0 + i];  // empty columns have tau = -inf
-                        const float est = est_of(acc[i], cc, fac, pcf);
-                        const float key = rank_key<kLB>(est, cc.epsnq, g1);
-                        if constexpr (kDump) {
-                            if (vok && col0 + i < it.ncols) {
-                                const int64_t di = (a.item_off[cc.pair] + (v >> 5)) * 32 + (v & 31);
-                                if (di < a.dump_cap) {
-                                    a.dump_ip[di] = -(int)acc[i];
-                                    a.dump_est[di] = est;
+                        const ColC& cc = cb[col0 + i];  // empty columns have tau = U = -inf
+                        bool sv;
+                        if constexpr (!kLB && !kRetry && !kDump) {
+                            const float ipn = __fsub_rn(__int_as_float(0x4B400000 + (int)acc[i]), 12582912.0f);
+                            const float tt = __fmaf_rn(-cc.a, ipn, __fmaf_rn(cc.b, pcf, -cc.K));
+                            sv = __fmaf_rn(-fac.y, tt, fac.x) <= cc.U;
+                        } else {
+                            const float est = est_of(acc[i], cc, fac, pcf);
+                            const float key = rank_key<kLB>(est, epsnq_of(cc), g1);
+                            if constexpr (kDump) {
+                                if (vok && col0 + i < it.ncols) {
+                                    const int64_t di = (a.item_off[cc.pair] + (v >> 5)) * 32 + (v & 31);
+                                    if (di < a.dump_cap) {
+                                        a.dump_ip[di] = -(int)acc[i];
+                                        a.dump_est[di] = est;
+                                    }
                                 }
                             }
-                        }
-                        bool sv;
-                        if constexpr (kRetry) {  // exact (key, row) <= tau64 (overflow / underflow re-scan)
-                            const uint32_t ko = f2o(key), to = f2o(cc.tau);
-                            sv = ko < to || (ko == to && row <= (uint32_t)cc.pair);
-                        } else {
-                            sv = key <= cc.tau;
+                            if constexpr (kRetry) {  // exact (key, row) <= tau64 (overflow / underflow re-scan)
+                                const uint32_t ko = f2o(key), to = f2o(cc.tau);
+                                sv = ko < to || (ko == to && row <= (uint32_t)cc.pair);
+                            } else {
+                                sv = key <= cc.tau;
+                            }
                         }
                         rowbits |= sv ? (1u << i) : 0u;
                     }
@@ -468,7 +480,7 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                             const uint32_t acci = tc::tmem_ld1(tcol + (uint32_t)i);
                             if ((bal >> lane) & 1u) {
                                 const ColC& cc = cb[col0 + i];
-                                const float key = rank_key<kLB>(est_of(acci, cc, fac, pcf), cc.epsnq, g1);
+                                const float key = rank_key<kLB>(est_of(acci, cc, fac, pcf), epsnq_of(cc), g1);
                                 const int pos = base + __popc(bal & ((1u << lane) - 1u));
                                 if (pos < a.cap) a.buf[(size_t)cc.q * a.cap + pos] = make_key(key, row);
                             }
@@ -540,13 +552,17 @@ __global__ void compact_flagged_kernel(const int* __restrict__ flags, int max_ra
 __global__ void colc_kernel(const int32_t* __restrict__ gpair, int64_t npairs, int nprobe, int D,
                             const float4* __restrict__ qscal, const float* __restrict__ tau,
                             const uint64_t* __restrict__ tau64, float eps0, const int64_t* __restrict__ dbase,
-                            const int64_t* __restrict__ doff, ColC* __restrict__ gcolc) {
+                            const int64_t* __restrict__ doff, const int32_t* __restrict__ probes,
+                            const float* __restrict__ list_amax, ColC* __restrict__ gcolc) {
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < npairs; g += (int64_t)gridDim.x * blockDim.x) {
         const int p = gpair[g];
         const int q = p / nprobe;
+        const PairC pc = pair_consts(qscal[p], D);
         ColC cc;
-        cc.c = pair_consts(qscal[p], D);
-        cc.epsnq = __fmul_rn(eps0, sqrtf(cc.c.nq2));
+        cc.a = pc.a;
+        cc.b = pc.b;
+        cc.K = pc.K;
+        cc.nq2 = pc.nq2;
         cc.q = q;
         if (dbase) {  // dense key dump: absolute offset of the pair's keys in (q, pair)
             const int64_t off = dbase[q] + doff[p];
@@ -559,6 +575,15 @@ __global__ void colc_kernel(const int32_t* __restrict__ gpair, int64_t npairs, i
         } else {
             cc.tau = tau[q];
             cc.pair = p;
+        }
+        // fast test bound: for est = RN(RN(A + nq2) - f t) <= tau, the fused
+        // RN(A - f t) exceeds tau - nq2 by at most a few ulps of A + nq2 + |tau|
+        if (cc.tau == INFINITY || cc.tau == -INFINITY) {
+            cc.U = cc.tau;
+        } else {
+            const float amax = list_amax[probes[p]];
+            const float mag = __fadd_rn(__fadd_rn(amax, pc.nq2), fabsf(cc.tau));
+            cc.U = __fadd_rn(__fsub_rn(cc.tau, pc.nq2), __fmul_rn(4.76837158e-7f, mag));  // 2^-21
         }
         gcolc[g] = cc;
     }
@@ -679,7 +704,7 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
     gcolc.alloc((size_t)a.npairs + kTN, st);
     colc_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((a.npairs + 255) / 256, 2048)), 256, 0, st>>>(
         a.gpair, a.npairs, a.nprobe, a.D, a.qscal, a.tau, retry ? a.tau64 : nullptr, a.eps0,
-        dense ? a.dense_base : nullptr, dense ? a.dense_off : nullptr, gcolc.p);
+        dense ? a.dense_base : nullptr, dense ? a.dense_off : nullptr, a.probes, a.list_amax, gcolc.p);
     RQ_CHECK_LAUNCH();
     a.gcolc = gcolc.p;
     int dev = 0, sms = 148;

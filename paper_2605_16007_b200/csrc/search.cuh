@@ -6,9 +6,10 @@
 namespace rabitq {
 
 struct ColC {      // per grouped row (query, list) constants of the grouped scan epilogue
-    PairC c;       // 16 B
+    float a, b, K; // PairC a, b, K (estimator)
+    float U;       // fast survivor test: A - f t <= U, U = tau - ||r_q||^2 + rounding margin
+    float nq2;     // ||r_q||^2
     float tau;     // threshold of the column's query
-    float epsnq;   // eps0 * n_q (lower-bound key)
     int q;         // query (-1: empty column)
     int pair;      // (query, probe) pair index
 };
@@ -46,6 +47,7 @@ struct ScanArgs {
     const int64_t* list_items; // [nlist + 1] prefix of (128-vector tile, 128-query group) items
     const uint16_t* pcnt;      // [nslots] popcount of each code
     const ColC* gcolc;         // [npairs] column constants in grouped order
+    const float* list_amax;    // [nlist] max n_o^2 of each list (fast-test margin)
     int experiment;            // diagnostics (RABITQ_IMMA_EXPERIMENT): 1 skip epilogue math, 2 skip UMMAs
     long long* trace;          // diagnostics (RABITQ_SCAN_TRACE): clock64 stamps of CTA 0, [trace_n][16]
     int trace_n;
