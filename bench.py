@@ -265,6 +265,7 @@ def run_ours(args):
         else:
             r = comm.search_sharded(idx, Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path)
         et.append(time.perf_counter() - t0)
+    log(f"[rank {rank}] e2e ms per call: {[round(t_ * 1e3, 2) for t_ in et]}")
     e2e_t = torch.tensor([sum(et)], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(e2e_t, op=torch.distributed.ReduceOp.MAX)
