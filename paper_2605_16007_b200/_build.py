@@ -40,7 +40,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return OUT
     inc, lib = _nccl_dirs()
     os.makedirs(OBJ, exist_ok=True)
-    common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+    extra = os.environ.get("RABITQ_NVCC_EXTRA", "").split()  # diagnostics, e.g. -DRABITQ_SCAN_TRACE
+    common = extra + ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
               "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc] + ARCH
 
     def compile_one(src):

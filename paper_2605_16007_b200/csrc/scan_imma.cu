@@ -324,11 +324,13 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                     {
                         const uint32_t aaddr = tmemA + (uint32_t)(s * kChunkCols);
                         const uint64_t bd = bdesc0 + (uint64_t)((c * bchunk) >> 4);
-                        const int n = (a.experiment & 2) ? ((c == 0) ? 1 : 0) : nks;
-                        for (int ks = 0; ks < n; ++ks)
-                            tc::mma_i8_ts_warp(dacc, aaddr + 8 * ks, bd + (uint64_t)(ks * 2), idesc,
-                                               (c > 0 || ks > 0) ? 1u : 0u);
-                        tc::commit_warp(&empty_bar[s]);                          // A slot s free once these retire
+                        if (a.experiment & 2) {  // diagnostics: skip the UMMAs
+                            if (c == 0) tc::mma_i8_ts_warp(dacc, aaddr, bd, idesc, 0u);
+                            tc::commit_warp(&empty_bar[s]);
+                        } else {
+                            // nks UMMAs + commit: A slot s free once these retire
+                            tc::mma_i8_ts_chunk(dacc, aaddr, bd, idesc, c > 0 ? 1u : 0u, nks, &empty_bar[s]);
+                        }
                         if (t == it.ntiles - 1) tc::commit_warp(&bfree_bar[c]);  // B chunk c free for the next item
                         if (c == nchunks - 1) tc::commit_warp(&accf_bar[b]);     // accumulator b complete
                         if (lane == 0) RQ_TR(10, gc);

@@ -195,6 +195,40 @@ __device__ __forceinline__ void mma_i8_ts_warp(uint32_t tmem_d, uint32_t tmem_a,
         "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// nk (1..4) UMMAs of consecutive 32-byte K steps (A: +8 TMEM columns, B
+// descriptor: +2 (32 bytes)) and the commit of `bar`, from a whole warp with one
+// election: the address increments stay inside the asm, so the operands cross
+// to uniform registers once per chunk instead of once per UMMA.
+__device__ __forceinline__ void mma_i8_ts_chunk(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                                uint32_t accumulate, int nk, uint64_t* bar) {
+#define RQ_MMA_HEAD                                   \
+    "{\n\t.reg .pred p, e, t;\n\t"                    \
+    ".reg .b32 a1, a2, a3;\n\t.reg .b64 b1, b2, b3;\n\t" \
+    "setp.ne.b32 p, %4, 0;\n\t"                        \
+    "setp.eq.b32 t, 0, 0;\n\t"                         \
+    "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t" \
+    "add.u64 b1, %2, 2;\n\tadd.u64 b2, %2, 4;\n\tadd.u64 b3, %2, 6;\n\t" \
+    "elect.sync _|e, 0xffffffff;\n\t"                  \
+    "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t"
+#define RQ_MMA_K1 "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %3, t;\n\t"
+#define RQ_MMA_K2 "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a2], b2, %3, t;\n\t"
+#define RQ_MMA_K3 "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a3], b3, %3, t;\n\t"
+#define RQ_MMA_TAIL "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t}"
+#define RQ_MMA_ARGS ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(smem_u32(bar)) : "memory"
+    switch (nk) {
+        case 1: asm volatile(RQ_MMA_HEAD RQ_MMA_TAIL RQ_MMA_ARGS); break;
+        case 2: asm volatile(RQ_MMA_HEAD RQ_MMA_K1 RQ_MMA_TAIL RQ_MMA_ARGS); break;
+        case 3: asm volatile(RQ_MMA_HEAD RQ_MMA_K1 RQ_MMA_K2 RQ_MMA_TAIL RQ_MMA_ARGS); break;
+        default: asm volatile(RQ_MMA_HEAD RQ_MMA_K1 RQ_MMA_K2 RQ_MMA_K3 RQ_MMA_TAIL RQ_MMA_ARGS); break;
+    }
+#undef RQ_MMA_HEAD
+#undef RQ_MMA_K1
+#undef RQ_MMA_K2
+#undef RQ_MMA_K3
+#undef RQ_MMA_TAIL
+#undef RQ_MMA_ARGS
+}
+
 __device__ __forceinline__ void commit_warp(uint64_t* bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\t"

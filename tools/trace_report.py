@@ -21,6 +21,9 @@ def stat(name, x):
 
 
 print(f"chunks traced {n}, tiles {nt}, span {c[n-1,4]-c[0,0]:.0f} cycles, per chunk {(c[n-1,4]-c[0,0])/n:.0f}")
+stat("prod: loop top -> issue done", c[:, 5] - c[:, 3])
+stat("prod: cp.async wait + LDS", c[:, 6] - c[:, 5])
+stat("prod: previous arrive -> loop top", c[1:, 3] - c[:-1, 4])
 stat("prod: wait slot", c[:, 1] - c[:, 0])
 stat("prod: expand + tcgen05.st", c[:, 2] - c[:, 1])
 stat("prod: bar + arrive", c[:, 4] - c[:, 2])
