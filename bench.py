@@ -139,12 +139,14 @@ def workload(args):
     return s
 
 
-def build_shard(s, rank, world, dev, rq):
+def build_shard(s, rank, world, dev, rq, proxy=None):
     from paper_2605_16007_b200 import dist as rdist
 
     """Generate this rank's contiguous id slice on the device and build its
-    shard (rank 0 trains P and the centroids, the others reuse them)."""
-    lo, hi = rdist.shard_range(s.N, rank, world)
+    shard (rank 0 trains P and the centroids, the others reuse them).
+    proxy = (r, G): a single process builds shard r of G exactly as rank 0
+    of a G-GPU job would build its own (CFG5 does not fit one GPU)."""
+    lo, hi = rdist.shard_range(s.N, *(proxy if proxy else (rank, world)))
     cen = synth.centres(s, dev)
     t0 = time.time()
     X = synth.base_rows(s, lo, hi, dev, cen=cen)
@@ -155,7 +157,7 @@ def build_shard(s, rank, world, dev, rq):
     tgen = time.time() - t0
     t0 = time.time()
     if world == 1:
-        idx = rq.Index(X, nlist=s.nlist, seed=s.build_seed, borrow=True, init_centroids=init)
+        idx = rq.Index(X, nlist=s.nlist, seed=s.build_seed, borrow=True, init_centroids=init, id_offset=lo)
     else:
         P = torch.empty(s.D, s.D, device=dev)
         C = torch.empty(s.nlist, s.D, device=dev)
@@ -189,7 +191,10 @@ def run_ours(args):
     if world > 1:
         torch.distributed.init_process_group("nccl", device_id=dev)
     s = workload(args)
-    idx, X, Q = build_shard(s, rank, world, dev, rq)
+    proxy = tuple(int(v) for v in args.shard.split("/")) if args.shard else None
+    if proxy and world > 1:
+        raise SystemExit("--shard is a single-process proxy")
+    idx, X, Q = build_shard(s, rank, world, dev, rq, proxy)
     comm = None
     if world > 1:
         uid = rdist.share_unique_id(rq.Comm.unique_id() if rank == 0 else None)
@@ -322,11 +327,13 @@ def run_ours(args):
         nsub = min(100 if s.N <= 10_000_000 else 20, s.nq)
         step = max(1, (1 << 28) // (s.D * 4 * 8))  # rows per chunk (~1 GiB of fp32 temporaries)
         gt = []
+        nx = X.shape[0]
+        lo = rdist.shard_range(s.N, *proxy)[0] if proxy else 0
         for q in range(nsub):
-            dd = torch.empty(s.N, dtype=torch.float64, device=dev)
-            for r0 in range(0, s.N, step):
+            dd = torch.empty(nx, dtype=torch.float64, device=dev)
+            for r0 in range(0, nx, step):
                 dd[r0:r0 + step] = (X[r0:r0 + step] - Q[q]).pow(2).sum(1, dtype=torch.float64)
-            gt.append(torch.topk(dd, s.k, largest=False).indices.cpu())
+            gt.append(torch.topk(dd, s.k, largest=False).indices.cpu() + lo)
         gt = torch.stack(gt).numpy()
         got = ids[:nsub].cpu().numpy()
         rec = float(np.mean([len(set(a_.tolist()) & set(b_.tolist())) / s.k for a_, b_ in zip(got, gt)]))
@@ -338,7 +345,8 @@ def run_ours(args):
                   else "u32 bit-planes (AND+POPC) + f32 estimator/re-rank"),
         "data": "synthetic (synth/ seeded Gaussian mixture, generated on device)",
         "config": {"workload": f"CFG{s.cfg}", "D": s.D, "N": s.N, "nlist": s.nlist, "nq": s.nq, "nprobe": s.nprobe,
-                   "k": s.k, "n_rerank": s.M, "kind": s.kind, "parallelism": f"list-shards x{world}",
+                   "k": s.k, "n_rerank": s.M, "kind": s.kind, "parallelism": (f"shard {args.shard} (single-GPU proxy: one rank's share)" if proxy
+                                   else f"list-shards x{world}"),
                    "l2": "flushed between steps (256 MiB write)", "scan_path": args.scan_path},
         "e2e": {"value": round(e2e_qps, 1), "unit": "queries/s", "h2d_bytes_per_step": s.nq * s.D * 4 * world,
                 "d2h_bytes_per_step": s.nq * s.k * 12 * world},
@@ -494,6 +502,8 @@ def main():
     ap.add_argument("--scan-path", type=int, default=0, dest="scan_path")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-recall", dest="recall", action="store_false")
+    ap.add_argument("--shard", default="", help="r/G: time shard r of G on one GPU (per-GPU proxy for configs "
+                    "that need G GPUs, e.g. CFG5); the line then reports that shard's QPS")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         log("note: warmup raised to the contract minimum of 3")
