@@ -131,6 +131,31 @@ __device__ __forceinline__ float rank_key(float est, float epsnq, float g1) {
 }
 
 // ------------------------------------------------------- warp primitives --
+// Blackwell packed FP32 (FADD2 / FFMA2 / FMUL2): two IEEE round-to-nearest
+// operations per instruction, each lane of the pair rounded exactly as the
+// scalar op would be
+#define RQ_F2_OP(name, op)                                                                                 \
+    __device__ __forceinline__ float2 name(float2 a, float2 b) {                                           \
+        float2 d;                                                                                          \
+        asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t" op    \
+            " rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"                                                    \
+            : "=f"(d.x), "=f"(d.y)                                                                         \
+            : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));                                                     \
+        return d;                                                                                          \
+    }
+RQ_F2_OP(fadd2, "add.rn.f32x2")
+RQ_F2_OP(fsub2, "sub.rn.f32x2")
+RQ_F2_OP(fmul2, "mul.rn.f32x2")
+#undef RQ_F2_OP
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "mov.b64 rc, {%6, %7};\n\tfma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+
 __device__ __forceinline__ int warp_sum(int v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
@@ -147,12 +172,53 @@ __device__ __forceinline__ float warp_sumf(float v) {
 // digit radix select with 8-bit digits (one histogram pass per digit,
 // early exit once the digit prefix is unique).  All NT threads must call.
 // Scratch: hist[256] + 4 words in shared memory.
+// The digits above the highest bit in which min and max differ are common to
+// all keys: one min/max pass skips them (and their single-bin histograms).
 template <int NT, typename KeyT, typename Get>
 __device__ KeyT block_select_kth(Get get, int n, int k, uint32_t* hist, uint32_t* sc) {
     constexpr int kBits = sizeof(KeyT) * 8;
+    static_assert(NT % 32 == 0 && NT / 32 <= 64, "block size");
     KeyT prefix = 0, mask = 0;
-    const int tid = threadIdx.x;
-    for (int shift = kBits - 8; shift >= 0; shift -= 8) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int shift0 = kBits - 8;
+    {
+        KeyT mn = ~(KeyT)0, mx = 0;
+        for (int i = tid; i < n; i += NT) {
+            const KeyT key = get(i);
+            mn = key < mn ? key : mn;
+            mx = key > mx ? key : mx;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const KeyT a = __shfl_xor_sync(0xFFFFFFFFu, mn, o), b = __shfl_xor_sync(0xFFFFFFFFu, mx, o);
+            mn = a < mn ? a : mn;
+            mx = b > mx ? b : mx;
+        }
+        KeyT* wr = reinterpret_cast<KeyT*>(hist);  // [2][NT / 32] (hist is free here)
+        __syncthreads();
+        if (lane == 0) {
+            wr[warp] = mn;
+            wr[NT / 32 + warp] = mx;
+        }
+        __syncthreads();
+        for (int w = 0; w < NT / 32; ++w) {
+            const KeyT a = wr[w], b = wr[NT / 32 + w];
+            mn = a < mn ? a : mn;
+            mx = b > mx ? b : mx;
+        }
+        __syncthreads();
+        const KeyT diff = mn ^ mx;
+        if (diff == 0) return mn;  // every key equal (n >= 1)
+        int hb;
+        if constexpr (sizeof(KeyT) == 8) hb = 63 - __clzll((long long)diff);
+        else hb = 31 - __clz((int)diff);
+        shift0 = (hb / 8) * 8;
+        if (shift0 + 8 < kBits) {
+            mask = ~(KeyT)0 << (shift0 + 8);
+            prefix = mn & mask;
+        }
+    }
+    for (int shift = shift0; shift >= 0; shift -= 8) {
         for (int i = tid; i < 256; i += NT) hist[i] = 0;
         __syncthreads();
         for (int i = tid; i < n; i += NT) {

@@ -118,6 +118,14 @@ __global__ __launch_bounds__(NT) void sgemm_kernel(int M, int N, int K, const fl
 void sgemm(int M, int N, int K, const float* A, int lda, const float* B, int ldb, bool b_trans, float* C,
            int ldc, int epi, const float* cn, cudaStream_t st) {
     if (M <= 0 || N <= 0) return;
+    // grid.y is limited to 65535 row tiles: taller products run as row slabs
+    constexpr int kSlab = 65535 * BM;
+    if (M > kSlab) {
+        for (int r0 = 0; r0 < M; r0 += kSlab)
+            sgemm(std::min(kSlab, M - r0), N, K, A + (size_t)r0 * lda, lda, B, ldb, b_trans, C + (size_t)r0 * ldc,
+                  ldc, epi, cn, st);
+        return;
+    }
     dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM);
     if (b_trans) {
         if (epi == 1) sgemm_kernel<true, 1><<<grid, NT, 0, st>>>(M, N, K, A, lda, B, ldb, C, ldc, cn);

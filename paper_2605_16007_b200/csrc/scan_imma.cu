@@ -80,7 +80,7 @@ __host__ __device__ inline SmemPlan smem_plan(int Dp) {
     int slots = (kTmemCols - 2 * (int)p.acc_cols) / kChunkCols;
     p.slots = slots < kMaxSlots ? slots : kMaxSlots;
     const uint32_t bres = (uint32_t)(p.nchunks * p.NG * kKC);
-    p.off_colc = bres;  // [2][NG] ColC
+    p.off_colc = bres;  // [2][NG / 2] ColPair
     p.off_raw = p.off_colc + 2u * p.NG * (uint32_t)sizeof(ColC);  // [kPF][128 rows][4 words]
     p.total = p.off_raw + (uint32_t)(kPF * kTM * 16) + 1024u;
     return p;
@@ -151,6 +151,41 @@ __device__ __forceinline__ float est_of(uint32_t acc, const ColC& cc, float2 fac
     return __fmaf_rn(-fac.y, tt, __fadd_rn(fac.x, cc.nq2));
 }
 
+// Column constants in shared memory, two columns per 64-byte record so that
+// the fast test of columns 2p, 2p+1 takes (-a, b) and (-K, U) of both with two
+// 16-byte loads, already paired for the packed FP32 ops (FFMA2 / FADD2)
+struct ColPair {
+    float na[2], b[2], nK[2], U[2];
+    float nq2[2], tau[2];
+    int q[2], pair[2];
+};
+__device__ __forceinline__ void colp_put(ColPair* cp, int c, const ColC& x) {
+    ColPair& P = cp[c >> 1];
+    const int h = c & 1;
+    P.na[h] = -x.a;
+    P.b[h] = x.b;
+    P.nK[h] = -x.K;
+    P.U[h] = x.U;
+    P.nq2[h] = x.nq2;
+    P.tau[h] = x.tau;
+    P.q[h] = x.q;
+    P.pair[h] = x.pair;
+}
+__device__ __forceinline__ ColC colp_get(const ColPair* cp, int c) {  // negations are exact
+    const ColPair& P = cp[c >> 1];
+    const int h = c & 1;
+    ColC x;
+    x.a = -P.na[h];
+    x.b = P.b[h];
+    x.K = -P.nK[h];
+    x.U = P.U[h];
+    x.nq2 = P.nq2[h];
+    x.tau = P.tau[h];
+    x.q = P.q[h];
+    x.pair = P.pair[h];
+    return x;
+}
+
 // eps0 n_q of a column (lower-bound rank key, R#15)
 #define epsnq_of(cc) __fmul_rn(a.eps0, sqrtf((cc).nq2))
 
@@ -203,7 +238,7 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
     uint8_t* smem = smem_raw + pad;
     const SmemPlan sp = smem_plan(a.Dp);
     uint8_t* Bres = smem;                                        // [nchunks][NG rows][128 B], 128-byte swizzle
-    ColC* colc = reinterpret_cast<ColC*>(smem + sp.off_colc);    // [2][NG]
+    ColPair* colc = reinterpret_cast<ColPair*>(smem + sp.off_colc);  // [2][NG / 2]
     __shared__ __align__(8) uint64_t full_bar[kMaxSlots], empty_bar[kMaxSlots], accf_bar[2], acce_bar[2],
         bfull_bar[kMaxChunks], bfree_bar[kMaxChunks];
     __shared__ uint32_t tmem_base_s;
@@ -382,11 +417,11 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
         if (item < total) {
             it = decode_item(a, NG, item);
             fetch_colc(it);
-            if (et < NG) colc[et] = nextc;
+            if (et < NG) colp_put(colc, et, nextc);
         }
         tc::named_barrier(1, kEpiWarps * 32);
         for (; item < total; item += gridDim.x, ++ic) {
-            const ColC* cb = colc + (ic & 1) * NG;
+            const ColPair* cb = colc + (ic & 1) * (NG / 2);
             // prefetch the next item's column constants (latency hidden by this item)
             const int64_t nitem = item + gridDim.x;
             Item nit{};
@@ -419,7 +454,7 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                         // the column's absolute offset rides in (q, pair)
 #pragma unroll
                         for (int i = 0; i < kEC; ++i) {
-                            const ColC& cc = cb[col0 + i];
+                            const ColC cc = colp_get(cb, col0 + i);
                             const float key = rank_key<kLB>(est_of(acc[i], cc, fac, pcf), epsnq_of(cc), g1);
                             const int64_t off = ((int64_t)(uint32_t)cc.pair << 32) | (uint32_t)cc.q;
                             if (vok && col0 + i < it.ncols) a.dense_keys[off + v] = f2o(key);
@@ -431,15 +466,30 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                     // rounding margin), a superset of est <= tau; phase 3 stores the
                     // exact keys.  Re-scan / lower-bound key / dump: the exact key.
                     uint32_t rowbits = 0u;
+                    if constexpr (!kLB && !kRetry && !kDump) {
+                        // packed: columns i, i + 1 per FADD2 / FFMA2, each lane rounded as
+                        // fma(-a, ipn, fma(b, pcf, -K)), fma(-f, t, A) (empty columns: U = -inf)
+                        const float2 pc2 = make_float2(pcf, pcf), nf2 = make_float2(-fac.y, -fac.y);
+                        const float2 fx2 = make_float2(fac.x, fac.x), mg2 = make_float2(12582912.0f, 12582912.0f);
+                        const float4* P0 = reinterpret_cast<const float4*>(cb + (col0 >> 1));  // col0 even
+#pragma unroll
+                        for (int i = 0; i < kEC; i += 2) {
+                            const float4* P = P0 + 2 * i;  // record (col0 + i) / 2 = 4 float4
+                            const float4 ab = P[0], ku = P[1];  // (-a0, -a1, b0, b1), (-K0, -K1, U0, U1)
+                            const float2 ipn = fsub2(make_float2(__int_as_float(0x4B400000 + (int)acc[i]),
+                                                                 __int_as_float(0x4B400000 + (int)acc[i + 1])), mg2);
+                            const float2 inner = ffma2(make_float2(ab.z, ab.w), pc2, make_float2(ku.x, ku.y));
+                            const float2 tt = ffma2(make_float2(ab.x, ab.y), ipn, inner);
+                            const float2 v = ffma2(nf2, tt, fx2);
+                            rowbits |= (v.x <= ku.z ? 1u : 0u) << i;
+                            rowbits |= (v.y <= ku.w ? 1u : 0u) << (i + 1);
+                        }
+                    } else {
 #pragma unroll
                     for (int i = 0; i < kEC; ++i) {
-                        const ColC& cc = cb[col0 + i];  // empty columns have tau = U = -inf
+                        const ColC cc = colp_get(cb, col0 + i);
                         bool sv;
-                        if constexpr (!kLB && !kRetry && !kDump) {
-                            const float ipn = __fsub_rn(__int_as_float(0x4B400000 + (int)acc[i]), 12582912.0f);
-                            const float tt = __fmaf_rn(-cc.a, ipn, __fmaf_rn(cc.b, pcf, -cc.K));
-                            sv = __fmaf_rn(-fac.y, tt, fac.x) <= cc.U;
-                        } else {
+                        {
                             const float est = est_of(acc[i], cc, fac, pcf);
                             const float key = rank_key<kLB>(est, epsnq_of(cc), g1);
                             if constexpr (kDump) {
@@ -460,6 +510,7 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                         }
                         rowbits |= sv ? (1u << i) : 0u;
                     }
+                    }
                     if (!vok) rowbits = 0u;
                     uint32_t cols = __reduce_or_sync(0xFFFFFFFFu, rowbits);
                     if (cols) {
@@ -472,7 +523,7 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                             if (lane == i) mybal = bal;
                         }
                         int mybase = 0;
-                        if (mybal) mybase = atomicAdd(&a.cnt[cb[col0 + (lane & (kEC - 1))].q], __popc(mybal));
+                        if (mybal) mybase = atomicAdd(&a.cnt[colp_get(cb, col0 + (lane & (kEC - 1))).q], __popc(mybal));
                         // phase 3: survivors re-read their accumulator column and store
                         // (key, row); same arithmetic as phase 1, same key
                         for (uint32_t m = cols; m; m &= m - 1) {
@@ -481,7 +532,7 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                             const int base = __shfl_sync(0xFFFFFFFFu, mybase, i);
                             const uint32_t acci = tc::tmem_ld1(tcol + (uint32_t)i);
                             if ((bal >> lane) & 1u) {
-                                const ColC& cc = cb[col0 + i];
+                                const ColC cc = colp_get(cb, col0 + i);
                                 const float key = rank_key<kLB>(est_of(acci, cc, fac, pcf), epsnq_of(cc), g1);
                                 const int pos = base + __popc(bal & ((1u << lane) - 1u));
                                 if (pos < a.cap) a.buf[(size_t)cc.q * a.cap + pos] = make_key(key, row);
@@ -496,7 +547,7 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
             }
             // publish the next item's column constants into the other buffer (its
             // last readers finished item ic - 1 before the previous barrier)
-            if (nitem < total && et < NG) colc[((ic + 1) & 1) * NG + et] = nextc;
+            if (nitem < total && et < NG) colp_put(colc + ((ic + 1) & 1) * (NG / 2), et, nextc);
             tc::named_barrier(1, kEpiWarps * 32);
             it = nit;
         }

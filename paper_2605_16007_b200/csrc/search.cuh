@@ -113,6 +113,10 @@ struct RerankArgs {
     const int64_t* dpos;
     const int64_t* list_off;
     const float* n_o;          // [nslots] ||o - c|| (the dense distances' error scale)
+    // row staging for the exact gather: each warp streams its candidates' rows
+    // into a private ring of `slots` shared-memory rows by bulk async copies
+    // (0: register loads; needs D % 4 == 0, D <= 1024, 16-byte aligned X)
+    int slots;
 };
 
 struct SearchCfg {

@@ -45,7 +45,9 @@ constexpr int kProdWarps = 8, kMmaWarp = 8, kEpiWarp0 = 9, kEpiWarps = 4;
 constexpr int kNT = (kEpiWarp0 + kEpiWarps) * 32;  // 416
 constexpr uint32_t kTmemCols = 2 * kBN;
 
-constexpr size_t kSmem = 1024 + (size_t)kRaw * (kRawA + kRawB) + (size_t)kSpl * (kSplA + kSplB) + 4 * kBM * 4;
+constexpr int kStg = 32 * 33;  // per epilogue warp: 32 x 32 output block, padded rows (row-major transpose)
+constexpr size_t kSmem = 1024 + (size_t)kRaw * (kRawA + kRawB) + (size_t)kSpl * (kSplA + kSplB) + 4 * kBM * 4 +
+                         (size_t)kEpiWarps * kStg * 4;
 
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
     return (1u << 4)                       // c_format: F32
@@ -127,6 +129,7 @@ __global__ __launch_bounds__(kNT, 1) void tgemm_kernel(const __grid_constant__ C
     uint8_t* splA = rawB + kRaw * kRawB;                      // [kSpl][hi, lo][canonical 128 x 16]
     uint8_t* splB = splA + kSpl * kSplA;                      // [kSpl][hi, lo][canonical 256 x 16]
     float* anorm = reinterpret_cast<float*>(splB + kSpl * kSplB);  // [2 buffers][2 halves][128] A row norm parts
+    float* stage = anorm + 4 * kBM;                                 // [kEpiWarps][32][33] store transpose
     __shared__ __align__(8) uint64_t full_bar[kSpl], empty_bar[kSpl], accf_bar[2], acce_bar[2], normf_bar[2],
         raw_bar[kRaw];
     __shared__ uint32_t tmem_base_s;
@@ -319,6 +322,36 @@ __global__ __launch_bounds__(kNT, 1) void tgemm_kernel(const __grid_constant__ C
             tc::mbar_wait(&normf_bar[b], ub & 1);
             float an = 0.0f;
             if constexpr (kEpi == TG_EPI_DIST) an = __fadd_rn(anorm[(b * 2) * kBM + r], anorm[(b * 2 + 1) * kBM + r]);
+            if constexpr (kEpi != TG_EPI_DIST) {
+                // row-major C: 32 x 32 blocks transposed through shared memory so
+                // that each store instruction writes 32 consecutive columns of a row
+                float* stg = stage + (warp - kEpiWarp0) * kStg;
+                for (int c0 = 0; c0 < ti.n; c0 += 32) {
+                    uint32_t acc[32];
+                    tc::tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * kBN + c0), acc);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) stg[lane * 33 + i] = __uint_as_float(acc[i]);
+                    __syncwarp();
+                    const int col = c0 + lane;
+                    const bool cok = col < ti.n;
+                    float bn = 0.0f;
+                    if constexpr (kEpi == TG_EPI_PROBE) bn = cok ? p.b_norm[ti.b0 + col] : 0.0f;
+                    const int rmax = min(32, ti.m - quarter * 32);
+                    for (int rr = 0; rr < rmax; ++rr) {
+                        const float v = stg[rr * 33 + lane];
+                        if (cok) {
+                            float* dst = p.C + ti.c0 + (int64_t)(quarter * 32 + rr) * ti.ldc + col;
+                            if constexpr (kEpi == TG_EPI_PROBE) *dst = __fmaf_rn(-2.0f, v, bn);
+                            else *dst = v;
+                        }
+                    }
+                    __syncwarp();
+                }
+                tc::fence_before_sync();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&acce_bar[b]);
+                continue;
+            }
             for (int c0 = 0; c0 < ti.n; c0 += 16) {
                 uint32_t acc[16];
                 tc::tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * kBN + c0), acc);

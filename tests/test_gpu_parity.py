@@ -202,6 +202,20 @@ def test_stage_parity(orc, D, N, nlist, nq, nprobe, k, M, scan_path):
     _stage_checks(orc, idx, X, Q, k, nprobe, M, scan_path=scan_path)
 
 
+@pytest.mark.parametrize("nlist,nprobe,nq", [(2048, 300, 40), (4096, 64, 300), (16384, 128, 64)])
+def test_probe_select_large_nlist(nlist, nprobe, nq, monkeypatch):
+    """Probe lists at large nlist (sampled-threshold select, search.cu
+    probe_select_big_kernel): the oracle's ranking of the GPU's own q' (L1),
+    and bit-identical to the radix select over the whole row."""
+    X, Q = make_data(32, 4 * nlist, nlist, nq)
+    idx = build(X, nlist)
+    _, _, a = debug_search(idx, Q, 10, nprobe, 50, dump=False)
+    pu.check_probe_lists(a["probes"], a["qrot"], idx.export()["centroids"], nprobe)
+    monkeypatch.setenv("RABITQ_PROBE_SELECT", "radix")
+    _, _, b = debug_search(idx, Q, 10, nprobe, 50, dump=False)
+    assert np.array_equal(a["probes"], b["probes"])
+
+
 @pytest.mark.parametrize("scan_path", [rq.SCAN_POPC, rq.SCAN_IMMA])
 def test_stage_parity_lower_bound_key(orc, scan_path):
     X, Q = make_data(128, 12000, 32, 8)

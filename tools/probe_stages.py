@@ -15,11 +15,17 @@ import synth  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--nq", type=int, default=0)
+ap.add_argument("--N", type=int, default=0, help="override the base size (probe/quantize stages do not depend on it)")
 ap.add_argument("--runs", default='[{}]', help="JSON list of search kwargs")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--profile-last", action="store_true", help="cudaProfilerStart/Stop around the last rep (ncu --profile-from-start off)")
 args = ap.parse_args()
-s = synth.spec(args.config, **({"nq": args.nq} if args.nq else {}))
+ov = {}
+if args.nq:
+    ov["nq"] = args.nq
+if args.N:
+    ov["N"] = args.N
+s = synth.spec(args.config, **ov)
 dev = torch.device("cuda", 0)
 cen = synth.centres(s, dev)
 X = synth.base_rows(s, 0, s.N, dev, cen=cen)
