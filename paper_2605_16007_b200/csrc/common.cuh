@@ -68,6 +68,31 @@ __host__ __device__ __forceinline__ U4 philox4x32_10(uint32_t k0, uint32_t k1, U
     return c;
 }
 
+// The same generator with the key schedule k_r = (k0 + r W0, k1 + r W1)
+// precomputed on the host: passed as a kernel parameter, the round keys are
+// constant-bank operands of the XORs (no per-call key bumps).
+struct PhiloxSched {
+    uint32_t k0[10], k1[10];
+};
+inline PhiloxSched philox_sched(uint32_t k0, uint32_t k1) {
+    PhiloxSched s;
+    for (int r = 0; r < 10; ++r) {
+        s.k0[r] = k0 + (uint32_t)r * 0x9E3779B9u;
+        s.k1[r] = k1 + (uint32_t)r * 0xBB67AE85u;
+    }
+    return s;
+}
+__device__ __forceinline__ U4 philox4x32_10(const PhiloxSched& s, U4 c) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = 0xD2511F53ull * c.x, p1 = 0xCD9E8D57ull * c.z;
+        const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        c = U4{hi1 ^ c.y ^ s.k0[r], lo1, hi0 ^ c.w ^ s.k1[r], lo0};
+    }
+    return c;
+}
+
 // --------------------------------------------------- order-preserving keys --
 __host__ __device__ __forceinline__ uint32_t f2o(float f) {
 #ifdef __CUDA_ARCH__
