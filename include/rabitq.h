@@ -171,6 +171,11 @@ typedef struct {
     int64_t n, id_offset, max_list;
     int64_t bytes_codes, bytes_factors, bytes_ids, bytes_vectors, bytes_total;
     int32_t vectors_borrowed;
+    /* derived copies built when they fit (both included in bytes_total):
+     * the codes expanded to s8 {0, -1} (the grouped tensor-core scan's A operand,
+     * loaded by TMA) and the vectors in slot order minus their centroid (the
+     * dense re-rank block); 0 when absent */
+    int64_t bytes_codes8, bytes_slot_vectors;
 } rabitq_index_info_t;
 rabitq_status rabitq_index_info(const rabitq_index* idx, rabitq_index_info_t* out);
 

@@ -106,6 +106,7 @@ class IndexInfo(ctypes.Structure):
         ("bytes_codes", ctypes.c_int64), ("bytes_factors", ctypes.c_int64), ("bytes_ids", ctypes.c_int64),
         ("bytes_vectors", ctypes.c_int64), ("bytes_total", ctypes.c_int64),
         ("vectors_borrowed", ctypes.c_int32),
+        ("bytes_codes8", ctypes.c_int64), ("bytes_slot_vectors", ctypes.c_int64),
     ]
 
 

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "index.cuh"
+#include "search.cuh"
 
 namespace rabitq {
 namespace {
@@ -301,6 +302,8 @@ void free_index_memory(rabitq_index* idx) {
     cudaFree(idx->X_owned);
     cudaFree(idx->Xs);
     idx->Xs = nullptr;
+    cudaFree(idx->codes8);
+    idx->codes8 = nullptr;
     cudaFree(idx->Corig);
     idx->Corig = nullptr;
     cudaFree(idx->list_amax);
@@ -549,6 +552,18 @@ void build_index(rabitq_index* idx, const float* X, int64_t n, int D, int nlist,
     list_amax_kernel<<<std::min(nlist, 4096), 256, 0, st>>>(idx->fac, idx->slot_off, idx->list_off, nlist,
                                                            idx->list_amax);
     RQ_CHECK_LAUNCH();
+
+    // ---- expanded codes: the grouped scan's A operand by TMA (when they fit comfortably) ----
+    {
+        const char* env = getenv("RABITQ_CODES8");  // "0": not built (the scan expands codes in the kernel)
+        size_t freeb = 0, totalb = 0;
+        RQ_CUDA(cudaMemGetInfo(&freeb, &totalb));
+        const size_t bytes = (size_t)(idx->nslots + 128) * 32 * W;
+        if (!(env && env[0] == '0') && W <= 32 && bytes <= (size_t)(0.25 * (double)freeb)) {
+            expand_codes(idx, st);
+            RQ_CUDA(cudaStreamSynchronize(st));
+        }
+    }
 
     // ---- slot-ordered vectors for the dense re-rank (when they fit comfortably) ----
     {

@@ -402,7 +402,10 @@ rabitq_status rabitq_index_info(const rabitq_index* idx, rabitq_index_info_t* ou
     out->bytes_factors = slots * (8 + 4 + 4 + 4);
     out->bytes_ids = slots * 4 + idx->n * 4;
     out->bytes_vectors = idx->borrowed ? 0 : idx->n * idx->D * 4;
+    out->bytes_codes8 = idx->codes8 ? slots * idx->W * 32 : 0;
+    out->bytes_slot_vectors = idx->Xs ? slots * idx->D * 4 : 0;
     out->bytes_total = out->bytes_codes + out->bytes_factors + out->bytes_ids + out->bytes_vectors +
+                       out->bytes_codes8 + out->bytes_slot_vectors +
                        (int64_t)idx->D * idx->D * 4 + (int64_t)idx->nlist * (idx->D + 1) * 4 +
                        (int64_t)(idx->nlist + 1) * 16;
     out->vectors_borrowed = idx->borrowed ? 1 : 0;

@@ -26,6 +26,9 @@ struct rabitq_index {
     int64_t* list_off = nullptr;   // [nlist + 1] list boundaries in list order (rank of vector)
     int64_t* slot_off = nullptr;   // [nlist + 1] 32-aligned slot starts
     uint32_t* codes = nullptr;     // [nslots / 32][W][32]
+    uint8_t* codes8 = nullptr;     // [nslots + 128][32 W] the codes as s8 {0, -1} in the grouped scan's K
+                                   // order (scan_imma.cu expand32), slot-major: its A operand by TMA;
+                                   // nullable (built when it fits)
     float2* fac = nullptr;         // [nslots] {n_o^2, 2 n_o / (rho sqrt(D))}
     uint16_t* pcnt = nullptr;      // [nslots] popcount of the code (grouped scan epilogue)
     float* list_amax = nullptr;    // [nlist] max n_o^2 of each list (grouped scan fast-test margin)

@@ -30,6 +30,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstring>
 #include <string>
 
 #include "search.cuh"
@@ -59,32 +60,59 @@ constexpr int kTmemCols = 512;
 constexpr int kPF = 8;                     // code-word prefetch ring (chunks in flight per producer thread)
 constexpr int kSmemLimit = 227 * 1024;
 
+// A operand by TMA (expanded codes in HBM, `ta`): A stages of one K chunk of a
+// 128-vector tile in shared memory instead of the TMEM A slots and producers
+constexpr int kAStage = kTM * kKC;  // 16 KB
+constexpr int kMinAStages = 3;
+
 // queries per group: all K chunks of a group fit the resident B region, and
-// the double-buffered accumulator leaves TMEM room for >= 2 A slots
-__host__ __device__ inline int group_cols(int Dp) {
+// the double-buffered accumulator leaves TMEM room for >= 2 A slots (ta: B
+// resident + >= 3 A stages + column constants fit shared memory; N <= 256)
+__host__ __device__ inline int group_cols(int Dp, bool ta) {
     const int nch = (Dp + kKC - 1) / kKC;
+    if (ta) {
+        int n = kTN;
+        while (n > kBoxRows && nch * n * kKC + kMinAStages * kAStage + 2 * n * (int)sizeof(ColC) + 2048 > kSmemLimit)
+            n -= kBoxRows;
+        return n;
+    }
     int n = (kBRes / (nch * kKC)) / kBoxRows * kBoxRows;
     return n > kMaxNG ? kMaxNG : n;
 }
 
-// shared-memory / TMEM plan of one launch (host and device agree)
+// shared-memory / TMEM plan of one launch (host and device agree); slots = TMEM
+// A slots, or (ta) shared-memory A stages
 struct SmemPlan {
     int nchunks, NG, slots;
     uint32_t acc_cols, off_colc, off_raw, total;
 };
-__host__ __device__ inline SmemPlan smem_plan(int Dp) {
+__host__ __device__ inline SmemPlan smem_plan(int Dp, bool ta) {
     SmemPlan p;
     p.nchunks = (Dp + kKC - 1) / kKC;
-    p.NG = group_cols(Dp);
+    p.NG = group_cols(Dp, ta);
     p.acc_cols = (uint32_t)((p.NG + 31) & ~31);  // per accumulator buffer
-    int slots = (kTmemCols - 2 * (int)p.acc_cols) / kChunkCols;
-    p.slots = slots < kMaxSlots ? slots : kMaxSlots;
     const uint32_t bres = (uint32_t)(p.nchunks * p.NG * kKC);
     p.off_colc = bres;  // [2][NG / 2] ColPair
+    if (ta) {
+        p.off_raw = (p.off_colc + 2u * p.NG * (uint32_t)sizeof(ColC) + 1023u) & ~1023u;  // A stages, 1024-aligned
+        int st = (int)(((uint32_t)kSmemLimit - 1024u - p.off_raw) / (uint32_t)kAStage);
+        p.slots = st < kMaxSlots ? st : kMaxSlots;
+        p.total = p.off_raw + (uint32_t)(p.slots * kAStage) + 1024u;
+        return p;
+    }
+    int slots = (kTmemCols - 2 * (int)p.acc_cols) / kChunkCols;
+    p.slots = slots < kMaxSlots ? slots : kMaxSlots;
     p.off_raw = p.off_colc + 2u * p.NG * (uint32_t)sizeof(ColC);  // [kPF][128 rows][4 words]
     p.total = p.off_raw + (uint32_t)(kPF * kTM * 16) + 1024u;
     return p;
 }
+
+// warp roles: (ta) no producers, a second loader warp streams A
+__host__ __device__ constexpr int mma_warp(bool ta) { return ta ? 0 : kProdWarps; }
+__host__ __device__ constexpr int load_warp(bool ta) { return mma_warp(ta) + 1; }
+__host__ __device__ constexpr int loada_warp(bool ta) { return mma_warp(ta) + 2; }
+__host__ __device__ constexpr int epi_warp0(bool ta) { return ta ? 3 : kProdWarps + 2; }
+__host__ __device__ constexpr int n_threads(bool ta) { return (epi_warp0(ta) + kEpiWarps) * 32; }
 
 struct Item {
     int j;
@@ -231,12 +259,16 @@ __device__ __forceinline__ void pos_next(const ScanArgs& a, int NG, int nchunks,
 //              item), chunk c of the next item as soon as chunk c is free
 //   warps 6-13 epilogue: tcgen05.ld the int32 inner products, fused
 //              estimator (+ bound), threshold, survivor append
-template <bool kLB, bool kDump, bool kRetry, bool kDense>
-__global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant__ CUtensorMap tmapB, ScanArgs a) {
+template <bool kLB, bool kDump, bool kRetry, bool kDense, bool kTA>
+__global__ __launch_bounds__(n_threads(kTA), 1) void scan_imma_kernel(const __grid_constant__ CUtensorMap tmapB,
+                                                                      const __grid_constant__ CUtensorMap tmapA,
+                                                                      ScanArgs a) {
+    constexpr int kMmaWarp = mma_warp(kTA), kLoadWarp = load_warp(kTA), kLoadAWarp = loada_warp(kTA),
+                  kEpiWarp0 = epi_warp0(kTA);
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
     uint8_t* smem = smem_raw + pad;
-    const SmemPlan sp = smem_plan(a.Dp);
+    const SmemPlan sp = smem_plan(a.Dp, kTA);
     uint8_t* Bres = smem;                                        // [nchunks][NG rows][128 B], 128-byte swizzle
     ColPair* colc = reinterpret_cast<ColPair*>(smem + sp.off_colc);  // [2][NG / 2]
     __shared__ __align__(8) uint64_t full_bar[kMaxSlots], empty_bar[kMaxSlots], accf_bar[2], acce_bar[2],
@@ -260,6 +292,7 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
             tc::mbar_init(&bfree_bar[c], 1);
         }
         tc::prefetch_tmap(&tmapB);
+        if (kTA) tc::prefetch_tmap(&tmapA);
     }
     tc::fence_before_sync();
     __syncthreads();
@@ -270,7 +303,7 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
     const int64_t total = a.list_items[a.nlist];
     const int bchunk = NG * kKC;  // bytes of one K chunk of the resident B
 
-    if (warp < kProdWarps) {
+    if (!kTA && warp < kProdWarps) {
         // ================= producers =================
         const int r = tid;  // tile row = vector = TMEM lane
         const int W = a.W;
@@ -357,13 +390,18 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                     tc::fence_after_sync();
                     if (lane == 0) RQ_TR(9, gc);
                     {
-                        const uint32_t aaddr = tmemA + (uint32_t)(s * kChunkCols);
                         const uint64_t bd = bdesc0 + (uint64_t)((c * bchunk) >> 4);
-                        if (a.experiment & 2) {  // diagnostics: skip the UMMAs
+                        if constexpr (kTA) {
+                            // A stage s (TMA, 128-byte swizzle) free once these retire
+                            const uint64_t ad = tc::smem_desc_sw128(tc::smem_u32(smem + sp.off_raw + s * kAStage));
+                            tc::mma_i8_ss_chunk(dacc, ad, bd, idesc, c > 0 ? 1u : 0u, nks, &empty_bar[s]);
+                        } else if (a.experiment & 2) {  // diagnostics: skip the UMMAs
+                            const uint32_t aaddr = tmemA + (uint32_t)(s * kChunkCols);
                             if (c == 0) tc::mma_i8_ts_warp(dacc, aaddr, bd, idesc, 0u);
                             tc::commit_warp(&empty_bar[s]);
                         } else {
                             // nks UMMAs + commit: A slot s free once these retire
+                            const uint32_t aaddr = tmemA + (uint32_t)(s * kChunkCols);
                             tc::mma_i8_ts_chunk(dacc, aaddr, bd, idesc, c > 0 ? 1u : 0u, nks, &empty_bar[s]);
                         }
                         if (t == it.ntiles - 1) tc::commit_warp(&bfree_bar[c]);  // B chunk c free for the next item
@@ -389,6 +427,24 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                     for (int bx = 0; bx < it.nboxes; ++bx)
                         tc::tma_load_2d(Bres + c * bchunk + bx * kBoxRows * kKC, &tmapB, &bfull_bar[c], c * kKC,
                                         (int)(it.grow0 + bx * kBoxRows));
+                }
+            }
+        }
+    } else if (kTA && warp == kLoadAWarp) {
+        // ================= code operand loader (A by TMA) =================
+        if (lane == 0) {
+            uint32_t gc = 0;
+            for (int64_t item = blockIdx.x; item < total; item += gridDim.x) {
+                const Item it = decode_item(a, NG, item);
+                for (int t = 0; t < it.ntiles; ++t) {
+                    const int row0 = (int)(it.slot_base + (it.t0 + t) * kTM);
+                    for (int c = 0; c < nchunks; ++c, ++gc) {
+                        const int s = (int)(gc % nsl);
+                        const uint32_t u = gc / nsl;
+                        if (u > 0) tc::mbar_wait_backoff(&empty_bar[s], (u - 1) & 1);
+                        tc::mbar_arrive_expect_tx(&full_bar[s], (uint32_t)kAStage);
+                        tc::tma_load_2d(smem + sp.off_raw + s * kAStage, &tmapA, &full_bar[s], c * kKC, row0);
+                    }
                 }
             }
         }
@@ -443,8 +499,19 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                 tc::mbar_wait(&accf_bar[b], ub & 1);
                 if (e == 0 && lane == 0) RQ_TR(14, tcnt);
                 tc::fence_after_sync();
-#pragma unroll 1
-                for (int hc = part; hc * kEC < ((a.experiment & 1) ? 0 : it.ncols); hc += kEpiWarps / 4) {
+                // pass A (each of this warp's column chunks): fast test, ballots and the
+                // chunk's counter atomics; pass B: the survivors' stores, after every
+                // atomic of the tile is in flight (their latency overlaps the tests)
+                constexpr int kMaxHC = (kTN / kEC + kEpiWarps / 4 - 1) / (kEpiWarps / 4);
+                uint32_t hc_cols[kMaxHC], hc_bal[kMaxHC];
+                int hc_base[kMaxHC];
+                const int ncols_e = (a.experiment & 1) ? 0 : it.ncols;
+#pragma unroll
+                for (int k = 0; k < kMaxHC; ++k) hc_cols[k] = 0u;
+#pragma unroll
+                for (int k = 0; k < kMaxHC; ++k) {
+                    const int hc = part + k * (kEpiWarps / 4);
+                    if (hc * kEC >= ncols_e) break;
                     const int col0 = hc * kEC;
                     const uint32_t tcol = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)b * sp.acc_cols + col0;
                     uint32_t acc[kEC];
@@ -512,7 +579,10 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                     }
                     }
                     if (!vok) rowbits = 0u;
-                    uint32_t cols = __reduce_or_sync(0xFFFFFFFFu, rowbits);
+                    const uint32_t cols = __reduce_or_sync(0xFFFFFFFFu, rowbits);
+                    hc_cols[k] = cols;
+                    hc_bal[k] = 0u;
+                    hc_base[k] = 0;
                     if (cols) {
                         // phase 2 (surviving columns only): lane i takes column i's ballot,
                         // then one atomic per column, all issued together
@@ -522,14 +592,23 @@ __global__ __launch_bounds__(kNT, 1) void scan_imma_kernel(const __grid_constant
                             const uint32_t bal = __ballot_sync(0xFFFFFFFFu, (rowbits >> i) & 1u);
                             if (lane == i) mybal = bal;
                         }
-                        int mybase = 0;
-                        if (mybal) mybase = atomicAdd(&a.cnt[colp_get(cb, col0 + (lane & (kEC - 1))).q], __popc(mybal));
+                        hc_bal[k] = mybal;
+                        if (mybal) hc_base[k] = atomicAdd(&a.cnt[colp_get(cb, col0 + (lane & (kEC - 1))).q], __popc(mybal));
+                    }
+                }
+                if constexpr (!kDense) {
+#pragma unroll
+                    for (int k = 0; k < kMaxHC; ++k) {
+                        const uint32_t cols = hc_cols[k];
+                        if (!cols) continue;
                         // phase 3: survivors re-read their accumulator column and store
                         // (key, row); same arithmetic as phase 1, same key
+                        const int col0 = (part + k * (kEpiWarps / 4)) * kEC;
+                        const uint32_t tcol = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)b * sp.acc_cols + col0;
                         for (uint32_t m = cols; m; m &= m - 1) {
                             const int i = __ffs(m) - 1;
-                            const uint32_t bal = __shfl_sync(0xFFFFFFFFu, mybal, i);
-                            const int base = __shfl_sync(0xFFFFFFFFu, mybase, i);
+                            const uint32_t bal = __shfl_sync(0xFFFFFFFFu, hc_bal[k], i);
+                            const int base = __shfl_sync(0xFFFFFFFFu, hc_base[k], i);
                             const uint32_t acci = tc::tmem_ld1(tcol + (uint32_t)i);
                             if ((bal >> lane) & 1u) {
                                 const ColC cc = colp_get(cb, col0 + i);
@@ -656,7 +735,34 @@ __global__ void list_items_kernel(int nlist, const int64_t* __restrict__ list_of
     }
 }
 
+// codes -> s8 {0, -1} rows in the K order of expand32 (the TMEM A operand the
+// producers would build), slot-major, 128 zero pad rows
+__global__ void expand_codes_kernel(const uint32_t* __restrict__ codes, int64_t nslots, int W,
+                                    uint4* __restrict__ out) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (nslots + kTM) * W;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = e / W;
+        const int w = (int)(e % W);
+        uint4 lo = make_uint4(0u, 0u, 0u, 0u), hi = lo;
+        if (s < nslots) expand32(__ldg(codes + ((s >> 5) * W + w) * 32 + (s & 31)), lo, hi);
+        out[2 * e] = lo;
+        out[2 * e + 1] = hi;
+    }
+}
+
 }  // namespace
+
+const uint8_t* codes8_of(const rabitq_index* idx) {
+    const char* env = getenv("RABITQ_CODES8");  // "0": expand in the kernel (diagnostics / tests)
+    return (env && env[0] == '0') ? nullptr : idx->codes8;
+}
+
+void expand_codes(rabitq_index* idx, cudaStream_t st) {
+    const size_t bytes = (size_t)(idx->nslots + kTM) * 32 * idx->W;
+    RQ_CUDA(cudaMalloc(&idx->codes8, bytes));
+    expand_codes_kernel<<<4096, 256, 0, st>>>(idx->codes, idx->nslots, idx->W, reinterpret_cast<uint4*>(idx->codes8));
+    RQ_CHECK_LAUNCH();
+}
 
 bool imma_wanted(const rabitq_index* idx, int64_t npairs, int scan_path) {
     if (scan_path == RABITQ_SCAN_POPC) return false;
@@ -694,7 +800,8 @@ void prepare_groups(const rabitq_index* idx, const int32_t* probes, int64_t n, c
     RQ_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, g.gcount.p, g.gstart.p, nlist + 1, st));
     group_fill_kernel<<<grid, 256, 0, st>>>(probes, sub, n, g.gstart.p, g.gfill.p, g.gpos.p, g.gpair.p);
     RQ_CHECK_LAUNCH();
-    list_items_kernel<<<(nlist + 256) / 256, 256, 0, st>>>(nlist, idx->list_off, g.gcount.p, group_cols(g.Dp),
+    list_items_kernel<<<(nlist + 256) / 256, 256, 0, st>>>(nlist, idx->list_off, g.gcount.p,
+                                                           group_cols(g.Dp, codes8_of(idx) != nullptr),
                                                            g.itemc.p);
     RQ_CHECK_LAUNCH();
     RQ_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb2, g.itemc.p, g.list_items.p, nlist + 1, st));
@@ -706,7 +813,8 @@ void group_items(const rabitq_index* idx, const int64_t* list_off, const Groups&
     const int nlist = idx->nlist;
     itemc.alloc((size_t)nlist + 1, st);
     items.alloc((size_t)nlist + 1, st);
-    list_items_kernel<<<(nlist + 256) / 256, 256, 0, st>>>(nlist, list_off, g.gcount.p, group_cols(g.Dp), itemc.p);
+    list_items_kernel<<<(nlist + 256) / 256, 256, 0, st>>>(nlist, list_off, g.gcount.p,
+                                                           group_cols(g.Dp, codes8_of(idx) != nullptr), itemc.p);
     RQ_CHECK_LAUNCH();
     size_t tb = 0;
     RQ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, itemc.p, items.p, nlist + 1, st));
@@ -773,16 +881,34 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
                                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     RQ_REQUIRE(cr == CUDA_SUCCESS, RABITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
-    const SmemPlan plan = smem_plan(a.Dp);
+    // A = expanded codes [(nslots + 128) x Dp] when the index has them: TMA box 128 bytes x 128 rows
+    const bool ta = a.codes8 != nullptr;
+    CUtensorMap tmapA;
+    std::memset(&tmapA, 0, sizeof(tmapA));
+    if (ta) {
+        const cuuint64_t adim[2] = {(cuuint64_t)a.Dp, (cuuint64_t)(a.nslots + kTM)};
+        const cuuint64_t astride[1] = {(cuuint64_t)a.Dp};
+        const cuuint32_t abox[2] = {(cuuint32_t)kKC, (cuuint32_t)kTM};
+        cr = get_encode()(&tmapA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(a.codes8), adim, astride, abox,
+                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        RQ_REQUIRE(cr == CUDA_SUCCESS, RABITQ_ERR_CUDA, "cuTensorMapEncodeTiled (A) failed: " + std::to_string((int)cr));
+    }
+    const SmemPlan plan = smem_plan(a.Dp, ta);
     RQ_REQUIRE(plan.slots >= 2 && plan.total <= (uint32_t)kSmemLimit, RABITQ_ERR_INTERNAL,
                "grouped scan: TMEM / shared-memory plan does not fit");
     const size_t smem = plan.total;
     const int grid = sms;
-#define RQ_IMMA4(LB, DP, RT, DN)                                                                               \
+#define RQ_IMMA5(LB, DP, RT, DN, TA)                                                                           \
     do {                                                                                                        \
-        RQ_CUDA(cudaFuncSetAttribute(scan_imma_kernel<LB, DP, RT, DN>,                                          \
+        RQ_CUDA(cudaFuncSetAttribute(scan_imma_kernel<LB, DP, RT, DN, TA>,                                      \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));                  \
-        scan_imma_kernel<LB, DP, RT, DN><<<grid, kNT, smem, st>>>(tmap, a);                                     \
+        scan_imma_kernel<LB, DP, RT, DN, TA><<<grid, n_threads(TA), smem, st>>>(tmap, tmapA, a);                \
+    } while (0)
+#define RQ_IMMA4(LB, DP, RT, DN)                \
+    do {                                        \
+        if (ta) RQ_IMMA5(LB, DP, RT, DN, true); \
+        else RQ_IMMA5(LB, DP, RT, DN, false);   \
     } while (0)
 #define RQ_IMMA(LB, DP, RT) RQ_IMMA4(LB, DP, RT, false)
     if (dense) {
@@ -800,6 +926,7 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
     }
 #undef RQ_IMMA
 #undef RQ_IMMA4
+#undef RQ_IMMA5
     RQ_CHECK_LAUNCH();
 }
 

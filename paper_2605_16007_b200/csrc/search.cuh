@@ -46,6 +46,8 @@ struct ScanArgs {
     const uint8_t* qbar8;      // [(npairs + 128) x Dp] quantized queries, grouped by list
     const int64_t* list_items; // [nlist + 1] prefix of (128-vector tile, 128-query group) items
     const uint16_t* pcnt;      // [nslots] popcount of each code
+    const uint8_t* codes8;     // [nslots + 128][Dp] expanded codes (nullable: expanded in the kernel)
+    int64_t nslots;
     const ColC* gcolc;         // [npairs] column constants in grouped order
     const float* list_amax;    // [nlist] max n_o^2 of each list (fast-test margin)
     int experiment;            // diagnostics (RABITQ_IMMA_EXPERIMENT): 1 skip epilogue math, 2 skip UMMAs
@@ -84,6 +86,10 @@ void prepare_groups(const rabitq_index* idx, const int32_t* probes, int64_t n, c
 int64_t regroup_flagged(const rabitq_index* idx, const int32_t* probes, int64_t npairs, int nprobe, const int* flags,
                         int max_rank, const Groups& full, Groups& sub, cudaStream_t st, int& launches);
 bool imma_wanted(const rabitq_index* idx, int64_t npairs, int scan_path);
+// build time: idx->codes8 (the grouped scan's A operand, loaded by TMA) when it fits
+void expand_codes(rabitq_index* idx, cudaStream_t st);
+// the expanded codes the grouped scan uses (nullptr: in-kernel expansion)
+const uint8_t* codes8_of(const rabitq_index* idx);
 
 struct RerankArgs {
     const int* cnt;

@@ -229,6 +229,38 @@ __device__ __forceinline__ void mma_i8_ts_chunk(uint32_t tmem_d, uint32_t tmem_a
 #undef RQ_MMA_ARGS
 }
 
+// The same with A in shared memory too (TMA-written, 128-byte swizzle, K-major):
+// both descriptors advance by 2 (32 bytes) per K step.
+__device__ __forceinline__ void mma_i8_ss_chunk(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                uint32_t accumulate, int nk, uint64_t* bar) {
+#define RQ_MMA_HEAD                                   \
+    "{\n\t.reg .pred p, e, t;\n\t"                    \
+    ".reg .b64 a1, a2, a3, b1, b2, b3;\n\t"            \
+    "setp.ne.b32 p, %4, 0;\n\t"                        \
+    "setp.eq.b32 t, 0, 0;\n\t"                         \
+    "add.u64 a1, %1, 2;\n\tadd.u64 a2, %1, 4;\n\tadd.u64 a3, %1, 6;\n\t" \
+    "add.u64 b1, %2, 2;\n\tadd.u64 b2, %2, 4;\n\tadd.u64 b3, %2, 6;\n\t" \
+    "elect.sync _|e, 0xffffffff;\n\t"                  \
+    "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
+#define RQ_MMA_K1 "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a1, b1, %3, t;\n\t"
+#define RQ_MMA_K2 "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a2, b2, %3, t;\n\t"
+#define RQ_MMA_K3 "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a3, b3, %3, t;\n\t"
+#define RQ_MMA_TAIL "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t}"
+#define RQ_MMA_ARGS ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(smem_u32(bar)) : "memory"
+    switch (nk) {
+        case 1: asm volatile(RQ_MMA_HEAD RQ_MMA_TAIL RQ_MMA_ARGS); break;
+        case 2: asm volatile(RQ_MMA_HEAD RQ_MMA_K1 RQ_MMA_TAIL RQ_MMA_ARGS); break;
+        case 3: asm volatile(RQ_MMA_HEAD RQ_MMA_K1 RQ_MMA_K2 RQ_MMA_TAIL RQ_MMA_ARGS); break;
+        default: asm volatile(RQ_MMA_HEAD RQ_MMA_K1 RQ_MMA_K2 RQ_MMA_K3 RQ_MMA_TAIL RQ_MMA_ARGS); break;
+    }
+#undef RQ_MMA_HEAD
+#undef RQ_MMA_K1
+#undef RQ_MMA_K2
+#undef RQ_MMA_K3
+#undef RQ_MMA_TAIL
+#undef RQ_MMA_ARGS
+}
+
 __device__ __forceinline__ void commit_warp(uint64_t* bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\t"

@@ -234,6 +234,27 @@ def test_scan_paths_identical(D):
     assert torch.equal(a_i, b_i) and torch.equal(a_d, b_d)
 
 
+@pytest.mark.parametrize("D", [96, 960])
+def test_scan_code_operand_paths_identical(D, monkeypatch):
+    """The grouped scan's A operand from the expanded codes in HBM (TMA) and
+    from the in-kernel expansion into TMEM (index built without the expanded
+    copy) give bit-identical results, including the debug dump of every ip and
+    estimate."""
+    X, Q = make_data(D, 40000 if D < 900 else 8000, 32, 256)
+    a = build(X, 32)
+    assert a.info()["bytes_codes8"] > 0
+    ai, ad, adbg = debug_search(a, Q[:64], 10, 8, 200, scan_path=rq.SCAN_IMMA)
+    si, sd = a.search(Q.cuda(), 10, 8, 200, scan_path=rq.SCAN_IMMA)
+    monkeypatch.setenv("RABITQ_CODES8", "0")  # the same index, codes expanded in the kernel
+    bi, bd, bdbg = debug_search(a, Q[:64], 10, 8, 200, scan_path=rq.SCAN_IMMA)
+    ti, td = a.search(Q.cuda(), 10, 8, 200, scan_path=rq.SCAN_IMMA)
+    assert np.array_equal(ai, bi) and np.array_equal(ad, bd)
+    assert np.array_equal(adbg["scan_ip"], bdbg["scan_ip"]) and np.array_equal(adbg["scan_est"], bdbg["scan_est"])
+    assert torch.equal(si, ti) and torch.equal(sd, td)
+    b = build(X, 32)  # built without the expanded copy
+    assert b.info()["bytes_codes8"] == 0
+
+
 def test_cfg1_end_to_end(orc):
     """CFG1 at full size (N = 1e5, D = 128, nlist 256, 100 queries, nprobe 16,
     k 10, M 100): GPU vs the oracle running the whole path independently (its
