@@ -491,6 +491,51 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_build(args):
+    """NEXT-3: index-build throughput as a second timed workload.
+    One build = rabitq_build over the config's N synthetic vectors resident in
+    HBM (k-means on the sampled training rows, rotation, assignment, encode,
+    list layout, the expanded codes and slot-ordered vectors when they fit).
+    The build is synchronous and host-orchestrated, so it is timed by the host
+    clock between device synchronizations."""
+    import paper_2605_16007_b200 as rq
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    s = workload(args)
+    cen = synth.centres(s, dev)
+    X = synth.base_rows(s, 0, s.N, dev, cen=cen)
+    init = synth.init_centroids(s, dev)
+    warm = max(1, min(args.warmup, 1))
+    steps = max(1, args.steps)
+    times = []
+    info = None
+    for i in range(warm + steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        idx = rq.Index(X, nlist=s.nlist, seed=s.build_seed, borrow=True, init_centroids=init)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        info = idx.info()
+        del idx
+        if i >= warm:
+            times.append(dt)
+        log(f"build {i}: {dt:.3f} s")
+    tb = float(np.mean(times))
+    line = {
+        "metric": "index build throughput", "value": round(s.N / tb, 1), "unit": "vectors/s", "n_gpus": 1,
+        "steps": steps, "warmup": warm, "ms_per_step": round(tb * 1e3, 2), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (k-means, rotation, assignment GEMMs) + u32 codes",
+        "data": "synthetic (synth/ seeded Gaussian mixture, generated on device)",
+        "config": {"workload": f"CFG{s.cfg} build", "D": s.D, "N": s.N, "nlist": s.nlist, "kind": s.kind,
+                   "kmeans": "25 Lloyd iterations on min(N, 256 nlist) stratified training rows",
+                   "timing": "host clock between device synchronizations (synchronous build)"},
+        "index_bytes": info["bytes_total"], "codes8_bytes": info["bytes_codes8"],
+        "slot_vector_bytes": info["bytes_slot_vectors"],
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -502,13 +547,17 @@ def main():
     ap.add_argument("--scan-path", type=int, default=0, dest="scan_path")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-recall", dest="recall", action="store_false")
+    ap.add_argument("--workload", choices=["search", "build"], default="search",
+                    help="build: time rabitq_build (NEXT-3) instead of the search hot path")
     ap.add_argument("--shard", default="", help="r/G: time shard r of G on one GPU (per-GPU proxy for configs "
                     "that need G GPUs, e.g. CFG5); the line then reports that shard's QPS")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         log("note: warmup raised to the contract minimum of 3")
         args.warmup = 3
-    if args.impl == "reference":
+    if args.workload == "build":
+        run_build(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

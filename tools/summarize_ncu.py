@@ -81,7 +81,8 @@ def full(rep, out_md, out_json):
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
             tot = rd * scale.get(m["dram__bytes_read.sum"][1], 1) + wr * scale.get(m["dram__bytes_write.sum"][1], 1)
             # the bench's dominant-kernel keys: the main scan launch and the re-rank
-            main_scan = ("scan_imma_kernel" in name and name.endswith("0, 0, 0, 0>")) or "scan_popc" in name
+            # scan_imma_kernel<LB, dump, retry, dense, tma-A>: the main scan has LB = dump = retry = dense = 0
+            main_scan = ("scan_imma_kernel<0, 0, 0, 0" in name) or "scan_popc" in name
             key = "scan" if main_scan else ("select_rerank" if "select_rerank" in name else name)
             js.setdefault(key, tot)
         except Exception:
