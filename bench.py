@@ -207,7 +207,7 @@ def run_ours(args):
     def step(prof=None):
         if comm is None:
             idx.search(Q, s.k, s.nprobe, s.M, scan_path=args.scan_path, stream=stream, out=(ids, dist),
-                       profile=prof)
+                       profile=prof, rerank=args.rerank)
         else:
             kw = dict(scan_path=args.scan_path, stream=stream.cuda_stream)
             if prof is not None:
@@ -257,7 +257,7 @@ def run_ours(args):
     dh = torch.empty(s.nq, s.k, dtype=torch.float32).pin_memory()
     for _ in range(1):
         if comm is None:
-            idx.search(Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path, out=(ih, dh))
+            idx.search(Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path, out=(ih, dh), rerank=args.rerank)
         else:
             comm.search_sharded(idx, Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path)
     barrier()
@@ -266,7 +266,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         if comm is None:
-            idx.search(Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path, out=(ih, dh))
+            idx.search(Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path, out=(ih, dh), rerank=args.rerank)
         else:
             r = comm.search_sharded(idx, Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path)
         et.append(time.perf_counter() - t0)
@@ -347,13 +347,16 @@ def run_ours(args):
         "config": {"workload": f"CFG{s.cfg}", "D": s.D, "N": s.N, "nlist": s.nlist, "nq": s.nq, "nprobe": s.nprobe,
                    "k": s.k, "n_rerank": s.M, "kind": s.kind, "parallelism": (f"shard {args.shard} (single-GPU proxy: one rank's share)" if proxy
                                    else f"list-shards x{world}"),
-                   "l2": "flushed between steps (256 MiB write)", "scan_path": args.scan_path},
+                   "l2": "flushed between steps (256 MiB write)", "scan_path": args.scan_path,
+                   **({"rerank": "bound-driven (NEXT-4)"} if args.rerank else {})},
         "e2e": {"value": round(e2e_qps, 1), "unit": "queries/s", "h2d_bytes_per_step": s.nq * s.D * 4 * world,
                 "d2h_bytes_per_step": s.nq * s.k * 12 * world},
         "gpu_launches": launches * args.steps,
         "roofline": roofline, "roofline_other": roofline_other, "scan": scan_roof,
         "stage_ms": {k_: round(v, 4) for k_, v in stage_ms.items()},
         "survivors_per_query": round(surv / s.nq, 1), "max_survivors": max_surv, "overflow_rescans": retries,
+        **({"reranked_per_query": round(float(np.mean([p["reranked"] for p in profs])) / s.nq, 1)}
+           if args.rerank else {}),
         "recall_at_k": rec, "clocks": clocks,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -547,6 +550,8 @@ def main():
     ap.add_argument("--scan-path", type=int, default=0, dest="scan_path")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-recall", dest="recall", action="store_false")
+    ap.add_argument("--rerank", type=int, default=0, choices=[0, 1],
+                    help="1: bound-driven re-rank set (NEXT-4; changes results, opt-in)")
     ap.add_argument("--workload", choices=["search", "build"], default="search",
                     help="build: time rabitq_build (NEXT-3) instead of the search hot path")
     ap.add_argument("--shard", default="", help="r/G: time shard r of G on one GPU (per-GPU proxy for configs "

@@ -90,6 +90,7 @@ void rabitq_build_opts_default(rabitq_build_opts* opts);
 /* --------------------------------------------------------------- search -- */
 typedef enum { RABITQ_SCAN_AUTO = 0, RABITQ_SCAN_POPC = 1, RABITQ_SCAN_IMMA = 2 } rabitq_scan_path;
 typedef enum { RABITQ_RANK_EST = 0, RABITQ_RANK_LOWER_BOUND = 1 } rabitq_rank_key;
+typedef enum { RABITQ_RERANK_FIXED = 0, RABITQ_RERANK_BOUND = 1 } rabitq_rerank_mode;
 
 /* Optional capture of the intermediate stages (parity harness).  Every
  * non-NULL member is filled (host or device memory); sizes in brackets. */
@@ -130,6 +131,7 @@ typedef struct {
     int32_t kernel_launches;        /* librabitq kernels launched by this call           */
     int32_t scan_path_used;         /* 1 popc, 2 imma                                    */
     int32_t batches;                /* internal query batches                            */
+    int64_t reranked;               /* candidates whose exact distance was taken (rerank 1) */
 } rabitq_profile;
 
 typedef struct {
@@ -147,6 +149,11 @@ typedef struct {
                                 in device memory are valid after that stream synchronizes     */
     rabitq_debug* debug;     /* nullable                                                       */
     rabitq_profile* profile; /* nullable, host memory                                          */
+    int32_t rerank;          /* 0: re-rank the n_rerank best estimates (default);
+                                1: bound-driven: of those, only the ones with
+                                est - bound <= the k-th smallest est + bound (bound = the
+                                estimator's error bound at eps0, NS(4)); changes results when a
+                                bound is violated at the boundary.  Requires rank_key EST. */
 } rabitq_search_opts;
 
 /* Search nq queries Q [nq x d] fp32: rotate, probe the nprobe

@@ -341,7 +341,12 @@ void oracle_estimate_fullq(const uint32_t* code, const double* rq, int D, double
 }
 
 /* ------------------------------------------------------------------------ */
-typedef struct { double key; int64_t id; double est; } cand_t;
+static int cmp_double(const void* pa, const void* pb) {
+    const double a = *(const double*)pa, b = *(const double*)pb;
+    return (a > b) - (a < b);
+}
+
+typedef struct { double key; int64_t id; double est; double bound; } cand_t;
 
 static int cmp_cand(const void* pa, const void* pb) {
     const cand_t* a = (const cand_t*)pa;
@@ -359,8 +364,9 @@ int oracle_search(const float* Q, int64_t nq, int D, const float* P, const float
                   int k, int nprobe, int M, uint64_t seed, int64_t qid_base, int rank_key,
                   double eps0, const float* qr_in, const int32_t* probes_in, int num_threads,
                   int64_t* ids, float* dists, int32_t* probes_out, int64_t* topm_ids,
-                  double* topm_est) {
+                  double* topm_est, int rerank_mode, int64_t* n_reranked) {
     if (nq < 0 || D < 1 || nlist < 1 || k < 1 || M < k || nprobe < 1 || nprobe > nlist) return -1;
+    if (rerank_mode != 0 && (rerank_mode != 1 || rank_key != 0)) return -1;
     const int W = (D + 31) / 32;
 #ifdef _OPENMP
     if (num_threads <= 0) num_threads = omp_get_max_threads();
@@ -402,6 +408,7 @@ int oracle_search(const float* Q, int64_t nq, int D, const float* P, const float
                                 Sq, nq2, eps0, &est, &bound);
                 cand[nc].key = (rank_key == 1) ? est - bound : est;
                 cand[nc].est = est;
+                cand[nc].bound = bound;
                 cand[nc].id = list_ids[s];
                 ++nc;
             }
@@ -415,14 +422,34 @@ int oracle_search(const float* Q, int64_t nq, int D, const float* P, const float
                 topm_est[(size_t)qi * M + i] = (i < m) ? cand[i].est : INFINITY;
             }
         }
+        /* O-S5b (rerank_mode 1, NEXT-4): bound-driven re-rank set.  With the
+         * error bound of Eq. (2)'s estimator (NS(4)), d lies in [est - bound,
+         * est + bound] at the bound's confidence; tau = the k-th smallest
+         * est + bound of the top-M; only candidates with est - bound <= tau can
+         * be in the top-k, the others are not re-ranked. */
+        uint8_t* keep = (uint8_t*)malloc(m > 0 ? (size_t)m : 1);
+        for (int64_t i = 0; i < m; ++i) keep[i] = 1;
+        if (rerank_mode == 1 && m > k) {
+            double* ub = (double*)malloc(sizeof(double) * (size_t)m);
+            for (int64_t i = 0; i < m; ++i) ub[i] = cand[i].est + cand[i].bound;
+            qsort(ub, m, sizeof(double), cmp_double);
+            const double tau = ub[k - 1];
+            for (int64_t i = 0; i < m; ++i) keep[i] = (cand[i].est - cand[i].bound <= tau);
+            free(ub);
+        }
         /* O-S6: exact squared L2 on the raw vectors, top-k by (d, id) (R#19) */
         dkey_t* fk = (dkey_t*)malloc(sizeof(dkey_t) * (m > 0 ? m : 1));
+        int64_t mr = 0;
         for (int64_t i = 0; i < m; ++i) {
+            if (!keep[i]) continue;
             const float* x = X + (size_t)(cand[i].id - id_offset) * D;
             double s = 0.0;
             for (int d = 0; d < D; ++d) { double t = (double)q[d] - (double)x[d]; s += t * t; }
-            fk[i].d = s; fk[i].id = cand[i].id;
+            fk[mr].d = s; fk[mr].id = cand[i].id; ++mr;
         }
+        if (n_reranked) n_reranked[qi] = mr;
+        free(keep);
+        m = mr;
         qsort(fk, m, sizeof(dkey_t), cmp_dkey);
         for (int i = 0; i < k; ++i) {
             ids[(size_t)qi * k + i] = (i < m) ? fk[i].id : -1;

@@ -23,6 +23,7 @@ LIB_PATH = os.path.join(_HERE, "librabitq.so")
 OK, ERR_INVALID_ARGUMENT, ERR_INVALID_DATA, ERR_OUT_OF_MEMORY, ERR_CUDA, ERR_NCCL, ERR_UNSUPPORTED, ERR_INTERNAL = range(8)
 SCAN_AUTO, SCAN_POPC, SCAN_IMMA = 0, 1, 2
 RANK_EST, RANK_LOWER_BOUND = 0, 1
+RERANK_FIXED, RERANK_BOUND = 0, 1
 
 
 class RabitqError(RuntimeError):
@@ -77,6 +78,7 @@ class Profile(ctypes.Structure):
         ("kernel_launches", ctypes.c_int32),
         ("scan_path_used", ctypes.c_int32),
         ("batches", ctypes.c_int32),
+        ("reranked", ctypes.c_int64),
     ]
 
     def as_dict(self):
@@ -96,6 +98,7 @@ class SearchOpts(ctypes.Structure):
         ("stream", ctypes.c_void_p),
         ("debug", ctypes.POINTER(Debug)),
         ("profile", ctypes.POINTER(Profile)),
+        ("rerank", ctypes.c_int32),
     ]
 
 
@@ -217,7 +220,7 @@ class Index:
     def search(self, Q, k: int, nprobe: int, n_rerank: int, *, scan_path: int = SCAN_AUTO,
                rank_key: int = RANK_EST, eps0: float = 0.0, query_id_base: int = 0, cap: int = 0,
                seed_max: int = 0, stream=None, debug: Optional[dict] = None, out=None,
-               profile: Optional[Profile] = None):
+               profile: Optional[Profile] = None, rerank: int = RERANK_FIXED):
         """Returns (ids int64 [nq, k], dists float32 [nq, k]) on Q's device.
         ``debug`` maps rabitq_debug member names to preallocated tensors."""
         torch = _torch()
@@ -232,6 +235,7 @@ class Index:
         lib().rabitq_search_opts_default(ctypes.byref(o))
         o.scan_path, o.rank_key, o.eps0 = scan_path, rank_key, eps0
         o.query_id_base, o.cap_per_query, o.seed_max = query_id_base, cap, seed_max
+        o.rerank = rerank
         o.stream = _stream_handle(stream)
         dbg = None
         if debug:

@@ -248,6 +248,9 @@ static void search_local(const rabitq_index* idx, const float* Q, int64_t nq, in
     rabitq::SearchCfg cfg;
     cfg.scan_path = o.scan_path;
     cfg.rank_key = o.rank_key;
+    RQ_REQUIRE(o.rerank == 0 || (o.rerank == 1 && o.rank_key == RABITQ_RANK_EST), RABITQ_ERR_INVALID_ARGUMENT,
+               "rerank must be 0 or 1 (1 requires rank_key EST)");
+    cfg.rerank = o.rerank;
     cfg.eps0 = o.eps0 > 0.0f ? o.eps0 : 1.9f;
     // the survivor buffer is cheap HBM (8 B/entry): size it so that overflow
     // re-scans are rare even when the seeded threshold is loose
@@ -324,6 +327,7 @@ static void search_local(const rabitq_index* idx, const float* Q, int64_t nq, in
         pf->kernel_launches = stats.launches;
         pf->scan_path_used = stats.used_imma ? 2 : 1;
         pf->batches = stats.batches;
+        pf->reranked = stats.reranked;
     }
     if (dg) {
         v_qbar.copy_back(st);

@@ -123,6 +123,9 @@ struct RerankArgs {
     // into a private ring of `slots` shared-memory rows by bulk async copies
     // (0: register loads; needs D % 4 == 0, D <= 1024, 16-byte aligned X)
     int slots;
+    // bound-driven re-rank set (NEXT-4): keep est - bound <= k-th smallest est + bound
+    int adaptive;
+    unsigned long long* reranked;  // [1] candidates kept, summed over queries (adaptive only)
 };
 
 struct SearchCfg {
@@ -132,6 +135,7 @@ struct SearchCfg {
     int cap = 0;
     int seed_max = 0;
     int refine_rank = 0;  // > 0: refine tau with a tensor-core pass over each query's nearest lists
+    int rerank = 0;       // 1: bound-driven re-rank set (NEXT-4)
 };
 
 struct DebugOut {  // device-or-host pointers (cudaMemcpyDefault), all nullable
@@ -156,6 +160,7 @@ struct SearchStats {
     int64_t survivors = 0;
     int64_t max_survivors = 0;
     int retries = 0;
+    int64_t reranked = 0;  // rerank 1: candidates re-ranked
     int launches = 0;
     int used_imma = 0;
     int batches = 0;

@@ -255,6 +255,46 @@ def test_scan_code_operand_paths_identical(D, monkeypatch):
     assert b.info()["bytes_codes8"] == 0
 
 
+@pytest.mark.parametrize("D,M", [(128, 100), (960, 400)])
+def test_adaptive_rerank_parity(orc, D, M):
+    """NEXT-4 (rerank = RERANK_BOUND): the GPU keeps exactly the top-M candidates
+    with est - bound <= the k-th smallest est + bound, computed here in fp32
+    from the GPU's own top-M capture (est, bound), and returns the oracle's
+    re-rank of that set; the profile counts the kept candidates.  Against the
+    oracle's independent adaptive search (fp64 decisions) the results agree
+    except where a decision sits on the fp32/fp64 boundary."""
+    X, Q = make_data(D, 20000 if D < 900 else 6000, 24, 32)
+    idx = build(X, 24)
+    k, nprobe = 10, 6
+    _, _, dbg = debug_search(idx, Q, k, nprobe, M, dump=False)
+    prof = rq.Profile()
+    ai, ad = idx.search(Q.cuda(), k, nprobe, M, rerank=rq.RERANK_BOUND, profile=prof)
+    ai, ad = ai.cpu().numpy(), ad.cpu().numpy()
+    tids, test, tb = dbg["topm_ids"], dbg["topm_est"], dbg["topm_bound"]
+    kept = np.full((Q.shape[0], M), -1, np.int64)
+    total = 0
+    for q in range(Q.shape[0]):
+        v = tids[q] >= 0
+        est, bnd = test[q][v].astype(np.float32), tb[q][v].astype(np.float32)
+        ub, lb = est + bnd, est - bnd
+        if v.sum() > k:
+            tau = np.sort(ub)[k - 1]
+            keep = lb <= tau
+        else:
+            keep = np.ones(v.sum(), bool)
+        s = tids[q][v][keep]
+        kept[q, :s.size] = s
+        total += s.size
+    assert prof.reranked == total
+    ri, rd = orc.rerank(Q.numpy(), X.numpy(), kept, k)
+    pu.check_final(ai, ad, ri, rd, k)
+    ex = idx.export()
+    oi, _ = orc.search(Q.numpy(), ex["rotation"], ex["centroids"], ex["list_off"], ex["ids"], ex["codes"],
+                       ex["n_o"], ex["rho"], X.numpy(), k, nprobe, M, SEED, rerank_mode=1)
+    agree = np.mean([len(set(a.tolist()) & set(b.tolist())) / k for a, b in zip(ai, oi)])
+    assert agree >= 0.98, agree
+
+
 def test_cfg1_end_to_end(orc):
     """CFG1 at full size (N = 1e5, D = 128, nlist 256, 100 queries, nprobe 16,
     k 10, M 100): GPU vs the oracle running the whole path independently (its

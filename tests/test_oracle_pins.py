@@ -588,3 +588,39 @@ def test_rerank_is_restricted_bruteforce(orc):
         s = sub[q][sub[q] >= 0]
         dd = ((X[s].astype(np.float64) - Q[q].astype(np.float64)) ** 2).sum(1)
         assert np.array_equal(ids2[q], s[np.lexsort((s, dd))][:5])
+
+
+# ------------------------------------------------- O-S5b, NEXT-4
+def test_adaptive_rerank_special_cases(orc):
+    """The bound-driven re-rank set (rerank_mode 1) against the modes it must
+    reduce to: an infinite bound keeps every top-M candidate (= the fixed-M
+    search); a zero bound keeps exactly the candidates whose estimate is <= the
+    k-th smallest estimate (= the fixed search with M = k, no ties here)."""
+    X, Q = _mixture(41, 3000, 32, 12, 20)
+    idx = orc.OracleIndex(X, 12, seed=5, max_iter=8)
+    k, M, nprobe = 10, 80, 4
+    ref_i, ref_d = idx.search(Q, k, nprobe, M)
+    nr = np.empty(20, np.int64)
+    a_i, a_d = idx.search(Q, k, nprobe, M, rerank_mode=1, eps0=1e30, n_reranked=nr)
+    assert np.array_equal(a_i, ref_i) and np.array_equal(a_d, ref_d) and np.all(nr == M)
+    k_i, k_d = idx.search(Q, k, nprobe, k)
+    z_i, z_d = idx.search(Q, k, nprobe, M, rerank_mode=1, eps0=0.0, n_reranked=nr)
+    assert np.array_equal(z_i, k_i) and np.array_equal(z_d, k_d) and np.all(nr == k)
+
+
+def test_adaptive_rerank_recall(orc):
+    """At the paper's confidence (eps0 = 1.9) the adaptive set keeps the fixed-M
+    result almost everywhere (a miss needs a bound violation at the boundary);
+    k <= re-ranked <= M, and a tighter bound never re-ranks more."""
+    X, Q = _mixture(42, 6000, 64, 16, 40)
+    idx = orc.OracleIndex(X, 16, seed=6, max_iter=8)
+    k, M, nprobe = 10, 200, 6
+    ref_i, _ = idx.search(Q, k, nprobe, M)
+    nr = np.empty(40, np.int64)
+    a_i, _ = idx.search(Q, k, nprobe, M, rerank_mode=1, n_reranked=nr)
+    agree = np.mean([len(set(a.tolist()) & set(b.tolist())) / k for a, b in zip(a_i, ref_i)])
+    assert agree >= 0.99, agree
+    assert np.all(nr >= k) and np.all(nr <= M)
+    nr2 = np.empty(40, np.int64)
+    idx.search(Q, k, nprobe, M, rerank_mode=1, eps0=0.5, n_reranked=nr2)
+    assert np.all(nr2 <= nr)
