@@ -207,7 +207,7 @@ def run_ours(args):
     def step(prof=None):
         if comm is None:
             idx.search(Q, s.k, s.nprobe, s.M, scan_path=args.scan_path, stream=stream, out=(ids, dist),
-                       profile=prof, rerank=args.rerank)
+                       profile=prof, rerank=args.rerank, query_bits=args.query_bits)
         else:
             kw = dict(scan_path=args.scan_path, stream=stream.cuda_stream)
             if prof is not None:
@@ -257,7 +257,8 @@ def run_ours(args):
     dh = torch.empty(s.nq, s.k, dtype=torch.float32).pin_memory()
     for _ in range(1):
         if comm is None:
-            idx.search(Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path, out=(ih, dh), rerank=args.rerank)
+            idx.search(Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path, out=(ih, dh), rerank=args.rerank,
+                       query_bits=args.query_bits)
         else:
             comm.search_sharded(idx, Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path)
     barrier()
@@ -266,7 +267,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         if comm is None:
-            idx.search(Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path, out=(ih, dh), rerank=args.rerank)
+            idx.search(Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path, out=(ih, dh), rerank=args.rerank,
+                       query_bits=args.query_bits)
         else:
             r = comm.search_sharded(idx, Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path)
         et.append(time.perf_counter() - t0)
@@ -341,14 +343,18 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": round(qps, 1), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": ("u8 (tcgen05 kind::i8: 0/1 codes x 4-bit query) + f32 estimator/re-rank" if imma
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": (("u8 (tcgen05 kind::i8: 0/1 codes x four 6-bit digit rows of the 24-bit fixed-point query)"
+                   if args.query_bits == 32 else "u8 (tcgen05 kind::i8: 0/1 codes x 4-bit query)")
+                  + " + f32 estimator/re-rank" if imma
                   else "u32 bit-planes (AND+POPC) + f32 estimator/re-rank"),
         "data": "synthetic (synth/ seeded Gaussian mixture, generated on device)",
         "config": {"workload": f"CFG{s.cfg}", "D": s.D, "N": s.N, "nlist": s.nlist, "nq": s.nq, "nprobe": s.nprobe,
                    "k": s.k, "n_rerank": s.M, "kind": s.kind, "parallelism": (f"shard {args.shard} (single-GPU proxy: one rank's share)" if proxy
                                    else f"list-shards x{world}"),
                    "l2": "flushed between steps (256 MiB write)", "scan_path": args.scan_path,
-                   **({"rerank": "bound-driven (NEXT-4)"} if args.rerank else {})},
+                   **({"rerank": "bound-driven (NEXT-4)"} if args.rerank else {}),
+                   **({"query": "unquantized, 24-bit fixed point digit rows (NEXT-1)"} if args.query_bits == 32
+                      else {})},
         "e2e": {"value": round(e2e_qps, 1), "unit": "queries/s", "h2d_bytes_per_step": s.nq * s.D * 4 * world,
                 "d2h_bytes_per_step": s.nq * s.k * 12 * world},
         "gpu_launches": launches * args.steps,
@@ -550,6 +556,8 @@ def main():
     ap.add_argument("--scan-path", type=int, default=0, dest="scan_path")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-recall", dest="recall", action="store_false")
+    ap.add_argument("--query-bits", type=int, default=4, choices=[4, 32], dest="query_bits",
+                    help="32: unquantized query (NEXT-1; changes the estimates, opt-in)")
     ap.add_argument("--rerank", type=int, default=0, choices=[0, 1],
                     help="1: bound-driven re-rank set (NEXT-4; changes results, opt-in)")
     ap.add_argument("--workload", choices=["search", "build"], default="search",

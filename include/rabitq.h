@@ -154,6 +154,11 @@ typedef struct {
                                 est - bound <= the k-th smallest est + bound (bound = the
                                 estimator's error bound at eps0, NS(4)); changes results when a
                                 bound is violated at the boundary.  Requires rank_key EST. */
+    int32_t query_bits;      /* 0 or 4: the 4-bit randomized query (NS(2), default); 32: the
+                                unquantized query: the estimator
+                                takes <x-bar, r_q> from r_q in 24-bit fixed point (error <= 1e-6
+                                n_o n_q), no Philox draws; grouped tensor-core scan only (d <= 1024,
+                                scan_path AUTO or IMMA), UNSUPPORTED otherwise */
 } rabitq_search_opts;
 
 /* Search nq queries Q [nq x d] fp32: rotate, probe the nprobe

@@ -179,8 +179,9 @@ def estimate_fullq(code, rq, D, n_o, rho, eps0=EPS0):
 
 def search(Q, P, Cr, list_off, list_ids, codes, n_o, rho, X, k, nprobe, M, seed, qid_base=0,
            id_offset=0, rank_key=0, eps0=EPS0, qr_in=None, probes_in=None, num_threads=0,
-           debug=False, rerank_mode=0, n_reranked=None):
-    """Full oracle search (O-S1..O-S6; rerank_mode 1 adds O-S5b, the
+           debug=False, rerank_mode=0, n_reranked=None, qmode=0):
+    """Full oracle search (O-S1..O-S6; qmode 1: the unquantized query, NEXT-1;
+    rerank_mode 1 adds O-S5b, the
     bound-driven re-rank set of SURVEY 8(f) NEXT-4).  Returns (ids, dists) or,
     with debug, (ids, dists, probes, topm_ids, topm_est).  n_reranked: optional
     int64 [nq] array receiving the number of candidates re-ranked per query."""
@@ -202,7 +203,7 @@ def search(Q, P, Cr, list_off, list_ids, codes, n_o, rho, X, k, nprobe, M, seed,
         _p(None if qr_in is None else _c(qr_in, np.float32)),
         _p(None if probes_in is None else _c(probes_in, np.int32)),
         ctypes.c_int(num_threads), _p(ids), _p(dists), _p(probes), _p(tids), _p(test),
-        ctypes.c_int(rerank_mode), _p(n_reranked),
+        ctypes.c_int(rerank_mode), _p(n_reranked), ctypes.c_int(qmode),
     ]
     # keep temporaries alive for the duration of the call
     keep = [a for a in args]

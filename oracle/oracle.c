@@ -364,8 +364,9 @@ int oracle_search(const float* Q, int64_t nq, int D, const float* P, const float
                   int k, int nprobe, int M, uint64_t seed, int64_t qid_base, int rank_key,
                   double eps0, const float* qr_in, const int32_t* probes_in, int num_threads,
                   int64_t* ids, float* dists, int32_t* probes_out, int64_t* topm_ids,
-                  double* topm_est, int rerank_mode, int64_t* n_reranked) {
+                  double* topm_est, int rerank_mode, int64_t* n_reranked, int qmode) {
     if (nq < 0 || D < 1 || nlist < 1 || k < 1 || M < k || nprobe < 1 || nprobe > nlist) return -1;
+    if (qmode != 0 && qmode != 1) return -1;
     if (rerank_mode != 0 && (rerank_mode != 1 || rank_key != 0)) return -1;
     const int W = (D + 31) / 32;
 #ifdef _OPENMP
@@ -396,16 +397,25 @@ int oracle_search(const float* Q, int64_t nq, int D, const float* P, const float
         for (int p = 0; p < nprobe; ++p) total += list_off[probes[p] + 1] - list_off[probes[p]];
         cand_t* cand = (cand_t*)malloc(sizeof(cand_t) * (total > 0 ? total : 1));
         int64_t nc = 0;
+        double* rq = (double*)malloc(sizeof(double) * D);
         for (int p = 0; p < nprobe; ++p) {
             const int j = probes[p];
             float vl, delta; int32_t Sq; double nq2;
-            oracle_quantize(qr, Cr + (size_t)j * D, D, seed, j, qid_base + qi, qbar, &vl, &delta, &Sq, &nq2);
+            if (qmode == 0)
+                oracle_quantize(qr, Cr + (size_t)j * D, D, seed, j, qid_base + qi, qbar, &vl, &delta, &Sq, &nq2);
+            else /* O-S3' (NEXT-1): the unquantized residual r_q = q' - c' */
+                for (int i = 0; i < D; ++i) rq[i] = (double)qr[i] - (double)Cr[(size_t)j * D + i];
             for (int64_t s = list_off[j]; s < list_off[j + 1]; ++s) {
-                int64_t pc;
-                int64_t ip = oracle_ip(codes + (size_t)s * W, qbar, D, &pc);
                 double est, bound;
-                oracle_estimate(ip, pc, D, (double)n_o[s], (double)rho_o[s], (double)vl, (double)delta,
-                                Sq, nq2, eps0, &est, &bound);
+                if (qmode == 0) {
+                    int64_t pc;
+                    int64_t ip = oracle_ip(codes + (size_t)s * W, qbar, D, &pc);
+                    oracle_estimate(ip, pc, D, (double)n_o[s], (double)rho_o[s], (double)vl, (double)delta,
+                                    Sq, nq2, eps0, &est, &bound);
+                } else {
+                    oracle_estimate_fullq(codes + (size_t)s * W, rq, D, (double)n_o[s], (double)rho_o[s], eps0,
+                                          &est, &bound);
+                }
                 cand[nc].key = (rank_key == 1) ? est - bound : est;
                 cand[nc].est = est;
                 cand[nc].bound = bound;
@@ -455,7 +465,7 @@ int oracle_search(const float* Q, int64_t nq, int D, const float* P, const float
             ids[(size_t)qi * k + i] = (i < m) ? fk[i].id : -1;
             dists[(size_t)qi * k + i] = (i < m) ? (float)fk[i].d : INFINITY;
         }
-        free(fk); free(cand); free(qbar); free(probes); free(qr);
+        free(fk); free(cand); free(qbar); free(probes); free(qr); free(rq);
     }
     return 0;
 }

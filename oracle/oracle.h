@@ -109,6 +109,8 @@ void oracle_estimate_fullq(const uint32_t* code, const double* rq, int D, double
  *   O-S3 quantize per (q, list)                  (Philox ctr uses qid_base + qi)
  *   O-S4 ip, est, bound for every vector of every probed list
  *   O-S5 top-M by (key, id), key = est (rank_key 0) or est - bound (rank_key 1)
+ *   qmode 1 (NEXT-1): no query quantization, est from <x-bar, r_q> with the exact
+ *        residual (oracle_estimate_fullq) instead of O-S3/O-S4's 4-bit form
  *   O-S5b rerank_mode 1 (NEXT-4, rank_key 0 only): keep the top-M candidates
  *        with est - bound <= tau, tau = k-th smallest est + bound; 0: keep all
  *   O-S6 exact squared L2 on raw vectors (fp64), top-k by (d, id); pad (-1, +inf)
@@ -125,7 +127,7 @@ int oracle_search(const float* Q, int64_t nq, int D, const float* P, const float
                   int k, int nprobe, int M, uint64_t seed, int64_t qid_base, int rank_key,
                   double eps0, const float* qr_in, const int32_t* probes_in, int num_threads,
                   int64_t* ids, float* dists, int32_t* probes_out, int64_t* topm_ids,
-                  double* topm_est, int rerank_mode, int64_t* n_reranked);
+                  double* topm_est, int rerank_mode, int64_t* n_reranked, int qmode);
 
 /* Fine ranking of given candidates (O-S6): exact squared L2 in fp64
  * between q and the raw vectors X[cand - id_offset] (cand = -1 skipped),

@@ -99,6 +99,7 @@ class SearchOpts(ctypes.Structure):
         ("debug", ctypes.POINTER(Debug)),
         ("profile", ctypes.POINTER(Profile)),
         ("rerank", ctypes.c_int32),
+        ("query_bits", ctypes.c_int32),
     ]
 
 
@@ -220,7 +221,7 @@ class Index:
     def search(self, Q, k: int, nprobe: int, n_rerank: int, *, scan_path: int = SCAN_AUTO,
                rank_key: int = RANK_EST, eps0: float = 0.0, query_id_base: int = 0, cap: int = 0,
                seed_max: int = 0, stream=None, debug: Optional[dict] = None, out=None,
-               profile: Optional[Profile] = None, rerank: int = RERANK_FIXED):
+               profile: Optional[Profile] = None, rerank: int = RERANK_FIXED, query_bits: int = 4):
         """Returns (ids int64 [nq, k], dists float32 [nq, k]) on Q's device.
         ``debug`` maps rabitq_debug member names to preallocated tensors."""
         torch = _torch()
@@ -236,6 +237,7 @@ class Index:
         o.scan_path, o.rank_key, o.eps0 = scan_path, rank_key, eps0
         o.query_id_base, o.cap_per_query, o.seed_max = query_id_base, cap, seed_max
         o.rerank = rerank
+        o.query_bits = query_bits
         o.stream = _stream_handle(stream)
         dbg = None
         if debug:

@@ -251,6 +251,11 @@ static void search_local(const rabitq_index* idx, const float* Q, int64_t nq, in
     RQ_REQUIRE(o.rerank == 0 || (o.rerank == 1 && o.rank_key == RABITQ_RANK_EST), RABITQ_ERR_INVALID_ARGUMENT,
                "rerank must be 0 or 1 (1 requires rank_key EST)");
     cfg.rerank = o.rerank;
+    RQ_REQUIRE(o.query_bits == 0 || o.query_bits == 4 || o.query_bits == 32, RABITQ_ERR_INVALID_ARGUMENT,
+               "query_bits must be 0 (4), 4 or 32");
+    cfg.full = o.query_bits == 32 ? 1 : 0;
+    RQ_REQUIRE(!cfg.full || (o.scan_path != RABITQ_SCAN_POPC && idx->W <= 32), RABITQ_ERR_UNSUPPORTED,
+               "query_bits 32 runs on the grouped tensor-core scan only (d <= 1024)");
     cfg.eps0 = o.eps0 > 0.0f ? o.eps0 : 1.9f;
     // the survivor buffer is cheap HBM (8 B/entry): size it so that overflow
     // re-scans are rare even when the seeded threshold is loose

@@ -214,6 +214,19 @@ __device__ __forceinline__ ColC colp_get(const ColPair* cp, int c) {  // negatio
     return x;
 }
 
+// the same estimator from a float ipn (= -ip): est_of(acc) == est_ipn(exact float of acc)
+__device__ __forceinline__ float est_ipn(float ipn, const ColC& cc, float2 fac, float pcf) {
+    const float tt = __fmaf_rn(-cc.a, ipn, __fmaf_rn(cc.b, pcf, -cc.K));
+    return __fmaf_rn(-fac.y, tt, __fadd_rn(fac.x, cc.nq2));
+}
+__device__ __forceinline__ float acc_f(uint32_t acc) {  // exact int32 -> float, |acc| < 2^22
+    return __fsub_rn(__int_as_float(0x4B400000 + (int)acc), 12582912.0f);
+}
+// NEXT-1: -sum_i b_i X_i from the four 6-bit digit accumulators (|acc_k| < 2^16)
+__device__ __forceinline__ float ipn_full(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3) {
+    return __fmaf_rn(262144.0f, acc_f(a3), __fmaf_rn(4096.0f, acc_f(a2), __fmaf_rn(64.0f, acc_f(a1), acc_f(a0))));
+}
+
 // eps0 n_q of a column (lower-bound rank key, R#15)
 #define epsnq_of(cc) __fmul_rn(a.eps0, sqrtf((cc).nq2))
 
@@ -259,7 +272,7 @@ __device__ __forceinline__ void pos_next(const ScanArgs& a, int NG, int nchunks,
 //              item), chunk c of the next item as soon as chunk c is free
 //   warps 6-13 epilogue: tcgen05.ld the int32 inner products, fused
 //              estimator (+ bound), threshold, survivor append
-template <bool kLB, bool kDump, bool kRetry, bool kDense, bool kTA>
+template <bool kLB, bool kDump, bool kRetry, bool kDense, bool kTA, bool kFull>
 __global__ __launch_bounds__(n_threads(kTA), 1) void scan_imma_kernel(const __grid_constant__ CUtensorMap tmapB,
                                                                       const __grid_constant__ CUtensorMap tmapA,
                                                                       ScanArgs a) {
@@ -516,13 +529,19 @@ __global__ __launch_bounds__(n_threads(kTA), 1) void scan_imma_kernel(const __gr
                     const uint32_t tcol = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)b * sp.acc_cols + col0;
                     uint32_t acc[kEC];
                     tc::tmem_ld16(tcol, acc);
+                    // kFull: a pair is 4 consecutive digit columns, logical column = its first
+                    constexpr int kStep = kFull ? 4 : 1;
+                    auto est_at = [&](int i, const ColC& cc) -> float {
+                        if constexpr (kFull) return est_ipn(ipn_full(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]), cc, fac, pcf);
+                        else return est_of(acc[i], cc, fac, pcf);
+                    };
                     if constexpr (kDense) {
                         // sample scan: every key, coalesced (lanes = consecutive vectors);
                         // the column's absolute offset rides in (q, pair)
 #pragma unroll
-                        for (int i = 0; i < kEC; ++i) {
+                        for (int i = 0; i < kEC; i += kStep) {
                             const ColC cc = colp_get(cb, col0 + i);
-                            const float key = rank_key<kLB>(est_of(acc[i], cc, fac, pcf), epsnq_of(cc), g1);
+                            const float key = rank_key<kLB>(est_at(i, cc), epsnq_of(cc), g1);
                             const int64_t off = ((int64_t)(uint32_t)cc.pair << 32) | (uint32_t)cc.q;
                             if (vok && col0 + i < it.ncols) a.dense_keys[off + v] = f2o(key);
                         }
@@ -533,7 +552,7 @@ __global__ __launch_bounds__(n_threads(kTA), 1) void scan_imma_kernel(const __gr
                     // rounding margin), a superset of est <= tau; phase 3 stores the
                     // exact keys.  Re-scan / lower-bound key / dump: the exact key.
                     uint32_t rowbits = 0u;
-                    if constexpr (!kLB && !kRetry && !kDump) {
+                    if constexpr (!kLB && !kRetry && !kDump && !kFull) {
                         // packed: columns i, i + 1 per FADD2 / FFMA2, each lane rounded as
                         // fma(-a, ipn, fma(b, pcf, -K)), fma(-f, t, A) (empty columns: U = -inf)
                         const float2 pc2 = make_float2(pcf, pcf), nf2 = make_float2(-fac.y, -fac.y);
@@ -553,17 +572,17 @@ __global__ __launch_bounds__(n_threads(kTA), 1) void scan_imma_kernel(const __gr
                         }
                     } else {
 #pragma unroll
-                    for (int i = 0; i < kEC; ++i) {
+                    for (int i = 0; i < kEC; i += kStep) {
                         const ColC cc = colp_get(cb, col0 + i);
                         bool sv;
                         {
-                            const float est = est_of(acc[i], cc, fac, pcf);
+                            const float est = est_at(i, cc);
                             const float key = rank_key<kLB>(est, epsnq_of(cc), g1);
                             if constexpr (kDump) {
                                 if (vok && col0 + i < it.ncols) {
                                     const int64_t di = (a.item_off[cc.pair] + (v >> 5)) * 32 + (v & 31);
                                     if (di < a.dump_cap) {
-                                        a.dump_ip[di] = -(int)acc[i];
+                                        a.dump_ip[di] = kFull ? 0 : -(int)acc[i];  // (full: ip exceeds int32)
                                         a.dump_est[di] = est;
                                     }
                                 }
@@ -610,9 +629,17 @@ __global__ __launch_bounds__(n_threads(kTA), 1) void scan_imma_kernel(const __gr
                             const uint32_t bal = __shfl_sync(0xFFFFFFFFu, hc_bal[k], i);
                             const int base = __shfl_sync(0xFFFFFFFFu, hc_base[k], i);
                             const uint32_t acci = tc::tmem_ld1(tcol + (uint32_t)i);
+                            uint32_t acc1 = 0u, acc2 = 0u, acc3 = 0u;
+                            if constexpr (kFull) {
+                                acc1 = tc::tmem_ld1(tcol + (uint32_t)i + 1u);
+                                acc2 = tc::tmem_ld1(tcol + (uint32_t)i + 2u);
+                                acc3 = tc::tmem_ld1(tcol + (uint32_t)i + 3u);
+                            }
                             if ((bal >> lane) & 1u) {
                                 const ColC cc = colp_get(cb, col0 + i);
-                                const float key = rank_key<kLB>(est_of(acci, cc, fac, pcf), epsnq_of(cc), g1);
+                                const float est = kFull ? est_ipn(ipn_full(acci, acc1, acc2, acc3), cc, fac, pcf)
+                                                        : est_of(acci, cc, fac, pcf);
+                                const float key = rank_key<kLB>(est, epsnq_of(cc), g1);
                                 const int pos = base + __popc(bal & ((1u << lane) - 1u));
                                 if (pos < a.cap) a.buf[(size_t)cc.q * a.cap + pos] = make_key(key, row);
                             }
@@ -638,29 +665,31 @@ __global__ __launch_bounds__(n_threads(kTA), 1) void scan_imma_kernel(const __gr
 
 // ------------------------------------------------------------ list grouping
 // pairs to group: all (sub == nullptr) or the listed pair indices
+// rows = grouped B rows per pair (1; 4 for the unquantized query's digit rows)
 __global__ void group_count_kernel(const int32_t* __restrict__ probes, const int32_t* __restrict__ sub, int64_t n,
-                                   int64_t* __restrict__ gcount) {
+                                   int64_t* __restrict__ gcount, int rows) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd((unsigned long long*)&gcount[probes[sub ? sub[i] : i]], 1ull);
+        atomicAdd((unsigned long long*)&gcount[probes[sub ? sub[i] : i]], (unsigned long long)rows);
 }
 
 __global__ void group_fill_kernel(const int32_t* __restrict__ probes, const int32_t* __restrict__ sub, int64_t n,
                                   const int64_t* __restrict__ gstart, int32_t* __restrict__ gfill,
-                                  int32_t* __restrict__ gpos, int32_t* __restrict__ gpair) {
+                                  int32_t* __restrict__ gpos, int32_t* __restrict__ gpair, int rows) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int p = sub ? sub[i] : (int)i;
         const int j = probes[p];
-        const int64_t pos = gstart[j] + atomicAdd(&gfill[j], 1);
-        gpos[i] = (int32_t)pos;
-        gpair[pos] = (int32_t)p;
+        const int64_t pos = gstart[j] + atomicAdd(&gfill[j], rows);
+        gpos[i] = (int32_t)pos;  // first of the pair's rows
+        for (int r = 0; r < rows; ++r) gpair[pos + r] = (int32_t)p;
     }
 }
 
 // copy the int8 query rows of the listed pairs from the full grouping into a sub grouping
+// (`rows` consecutive rows of Dp bytes per pair)
 __global__ void gather_rows_kernel(const int32_t* __restrict__ sub, int64_t n, const int32_t* __restrict__ gpos_full,
                                    const uint8_t* __restrict__ q8_full, const int32_t* __restrict__ gpos_sub,
-                                   uint8_t* __restrict__ q8_sub, int Dp) {
-    const int per = Dp / 16;
+                                   uint8_t* __restrict__ q8_sub, int Dp, int rows) {
+    const int per = rows * Dp / 16;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * per; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = e / per;
         const int k = (int)(e % per);
@@ -773,23 +802,24 @@ bool imma_wanted(const rabitq_index* idx, int64_t npairs, int scan_path) {
 }
 
 void prepare_groups(const rabitq_index* idx, const int32_t* probes, int64_t n, const int32_t* sub, Groups& g,
-                    cudaStream_t st, int& launches) {
+                    cudaStream_t st, int& launches, int rows) {
     const int nlist = idx->nlist;
     g.Dp = ((idx->D + 31) / 32) * 32;
     g.n = n;
+    g.rows = rows;
     g.gcount.alloc((size_t)nlist + 1, st);
     g.gstart.alloc((size_t)nlist + 1, st);
     g.itemc.alloc((size_t)nlist + 1, st);
     g.list_items.alloc((size_t)nlist + 1, st);
     g.gfill.alloc((size_t)nlist, st);
     g.gpos.alloc((size_t)n, st);
-    g.gpair.alloc((size_t)n + kTN, st);
-    g.qbar8.alloc(((size_t)n + kTN) * g.Dp, st);
+    g.gpair.alloc((size_t)n * rows + kTN, st);
+    g.qbar8.alloc(((size_t)n * rows + kTN) * g.Dp, st);
     RQ_CUDA(cudaMemsetAsync(g.gcount.p, 0, ((size_t)nlist + 1) * sizeof(int64_t), st));
     RQ_CUDA(cudaMemsetAsync(g.gfill.p, 0, (size_t)nlist * sizeof(int32_t), st));
-    RQ_CUDA(cudaMemsetAsync(g.gpair.p + n, 0, kTN * sizeof(int32_t), st));
+    RQ_CUDA(cudaMemsetAsync(g.gpair.p + n * rows, 0, kTN * sizeof(int32_t), st));
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 2048));
-    group_count_kernel<<<grid, 256, 0, st>>>(probes, sub, n, g.gcount.p);
+    group_count_kernel<<<grid, 256, 0, st>>>(probes, sub, n, g.gcount.p, rows);
     RQ_CHECK_LAUNCH();
     size_t tb = 0;
     RQ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, g.gcount.p, g.gstart.p, nlist + 1, st));
@@ -798,7 +828,7 @@ void prepare_groups(const rabitq_index* idx, const int32_t* probes, int64_t n, c
     WBuf<uint8_t> tmp;
     tmp.alloc(std::max(tb, tb2), st);
     RQ_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, g.gcount.p, g.gstart.p, nlist + 1, st));
-    group_fill_kernel<<<grid, 256, 0, st>>>(probes, sub, n, g.gstart.p, g.gfill.p, g.gpos.p, g.gpair.p);
+    group_fill_kernel<<<grid, 256, 0, st>>>(probes, sub, n, g.gstart.p, g.gfill.p, g.gpos.p, g.gpair.p, rows);
     RQ_CHECK_LAUNCH();
     list_items_kernel<<<(nlist + 256) / 256, 256, 0, st>>>(nlist, idx->list_off, g.gcount.p,
                                                            group_cols(g.Dp, codes8_of(idx) != nullptr),
@@ -838,10 +868,10 @@ int64_t regroup_flagged(const rabitq_index* idx, const int32_t* probes, int64_t 
     RQ_CUDA(cudaMemcpyAsync(&n, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     RQ_CUDA(cudaStreamSynchronize(st));
     if (n == 0) return 0;
-    prepare_groups(idx, probes, n, list.p, sub, st, launches);
-    const int per = full.Dp / 16;
+    prepare_groups(idx, probes, n, list.p, sub, st, launches, full.rows);
+    const int per = full.rows * full.Dp / 16;
     gather_rows_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(((int64_t)n * per + 255) / 256, 4096)), 256,
-                         0, st>>>(list.p, n, full.gpos.p, full.qbar8.p, sub.gpos.p, sub.qbar8.p, full.Dp);
+                         0, st>>>(list.p, n, full.gpos.p, full.qbar8.p, sub.gpos.p, sub.qbar8.p, full.Dp, full.rows);
     RQ_CHECK_LAUNCH();
     launches += 2;
     return n;
@@ -899,11 +929,16 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
                "grouped scan: TMEM / shared-memory plan does not fit");
     const size_t smem = plan.total;
     const int grid = sms;
-#define RQ_IMMA5(LB, DP, RT, DN, TA)                                                                           \
+#define RQ_IMMA6(LB, DP, RT, DN, TA, FU)                                                                       \
     do {                                                                                                        \
-        RQ_CUDA(cudaFuncSetAttribute(scan_imma_kernel<LB, DP, RT, DN, TA>,                                      \
+        RQ_CUDA(cudaFuncSetAttribute(scan_imma_kernel<LB, DP, RT, DN, TA, FU>,                                  \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));                  \
-        scan_imma_kernel<LB, DP, RT, DN, TA><<<grid, n_threads(TA), smem, st>>>(tmap, tmapA, a);                \
+        scan_imma_kernel<LB, DP, RT, DN, TA, FU><<<grid, n_threads(TA), smem, st>>>(tmap, tmapA, a);            \
+    } while (0)
+#define RQ_IMMA5(LB, DP, RT, DN, TA)                   \
+    do {                                               \
+        if (a.full) RQ_IMMA6(LB, DP, RT, DN, TA, true);  \
+        else RQ_IMMA6(LB, DP, RT, DN, TA, false);        \
     } while (0)
 #define RQ_IMMA4(LB, DP, RT, DN)                \
     do {                                        \
@@ -927,6 +962,7 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
 #undef RQ_IMMA
 #undef RQ_IMMA4
 #undef RQ_IMMA5
+#undef RQ_IMMA6
     RQ_CHECK_LAUNCH();
 }
 

@@ -58,6 +58,7 @@ struct ScanArgs {
     uint32_t* dense_keys;
     const int64_t* dense_base;  // [nq] first key of each query
     const int64_t* dense_off;   // [npairs] offset of each (query, probe) pair within its query
+    int full;                   // 1: unquantized query (NEXT-1), 4 digit rows per pair (npairs = rows)
 };
 
 template <typename T>
@@ -79,10 +80,11 @@ struct Groups {
     WBuf<int32_t> gfill, gpos, gpair;
     WBuf<uint8_t> qbar8;
     int Dp = 0;
-    int64_t n = 0;  // grouped rows
+    int64_t n = 0;  // grouped pairs
+    int rows = 1;   // B rows per pair (4: the unquantized query's digit rows, NEXT-1)
 };
 void prepare_groups(const rabitq_index* idx, const int32_t* probes, int64_t n, const int32_t* sub, Groups& g,
-                    cudaStream_t st, int& launches);
+                    cudaStream_t st, int& launches, int rows = 1);
 int64_t regroup_flagged(const rabitq_index* idx, const int32_t* probes, int64_t npairs, int nprobe, const int* flags,
                         int max_rank, const Groups& full, Groups& sub, cudaStream_t st, int& launches);
 bool imma_wanted(const rabitq_index* idx, int64_t npairs, int scan_path);
@@ -136,6 +138,7 @@ struct SearchCfg {
     int seed_max = 0;
     int refine_rank = 0;  // > 0: refine tau with a tensor-core pass over each query's nearest lists
     int rerank = 0;       // 1: bound-driven re-rank set (NEXT-4)
+    int full = 0;         // 1: unquantized query (NEXT-1), grouped tensor-core scan
 };
 
 struct DebugOut {  // device-or-host pointers (cudaMemcpyDefault), all nullable

@@ -295,6 +295,58 @@ def test_adaptive_rerank_parity(orc, D, M):
     assert agree >= 0.98, agree
 
 
+@pytest.mark.parametrize("D,N,nlist,nq,nprobe,k,M", [
+    (128, 20000, 64, 12, 8, 10, 100),
+    (96, 15000, 48, 10, 6, 10, 200),
+    (960, 6000, 16, 4, 4, 100, 1000),
+    (33, 4000, 10, 8, 3, 5, 40),
+])
+def test_fullq_parity(orc, D, N, nlist, nq, nprobe, k, M):
+    """NEXT-1 (query_bits = 32): every scanned estimate within the estimator
+    tolerance of the oracle's exact-residual estimator (estimate_fullq, fp64,
+    on the GPU's own q' and probes), the top-M equal to the oracle's qmode-1
+    search except inside the tie band, and the final top-k = the oracle's
+    re-rank of the GPU's top-M."""
+    X, Q = make_data(D, N, nlist, nq)
+    idx = build(X, nlist)
+    ids, d, dbg = debug_search(idx, Q, k, nprobe, M, query_bits=32)
+    ex = idx.export()
+    Cr, off, lids, codes, n_o, rho = ex["centroids"], ex["list_off"], ex["ids"], ex["codes"], ex["n_o"], ex["rho"]
+    qr, probes = dbg["qrot"], dbg["probes"]
+    pu.check_probe_lists(probes, qr, Cr, nprobe)
+    pair, lst, pos, valid, nitems = pu.list_pos_of_items(probes.reshape(-1), off)
+    sest = dbg["scan_est"][: nitems * 32]
+    e = np.nonzero(valid)[0]
+    row = off[lst[e]] + pos[e]
+    rng = np.random.default_rng(0)
+    pick = e.size if e.size <= 20000 else 20000
+    sel = rng.choice(e.size, size=pick, replace=False)
+    for t_ in sel:
+        p_ = int(pair[e[t_]])
+        q_, pp = divmod(p_, nprobe)
+        rq = qr[q_].astype(np.float64) - Cr[int(probes[q_, pp])].astype(np.float64)
+        est, _ = orc.estimate_fullq(codes[row[t_]], rq, D, float(n_o[row[t_]]), float(rho[row[t_]]))
+        tol = pu.est_tol(float(n_o[row[t_]]), float((rq * rq).sum()))
+        assert abs(float(sest[e[t_]]) - est) <= tol, (t_, sest[e[t_]], est, tol)
+    oi, od, _, tids, test = orc.search(Q.numpy(), ex["rotation"], Cr, off, lids, codes, n_o, rho, X.numpy(), k,
+                                       nprobe, M, SEED, qr_in=qr, probes_in=probes, debug=True, qmode=1)
+    gt = dbg["topm_ids"]
+    for q in range(nq):
+        a, b = set(gt[q][gt[q] >= 0].tolist()), set(tids[q][tids[q] >= 0].tolist())
+        if a == b:
+            continue
+        mth = test[q][np.isfinite(test[q])].max()
+        band = 4 * pu.EST_REL * float(np.sqrt(((qr[q][None] - Cr[probes[q]]) ** 2).sum(1)).max()) * float(n_o.max())
+        for x in a ^ b:
+            r_ = int(np.nonzero(lids == x)[0][0])
+            j = int(np.searchsorted(off, r_, side="right") - 1)
+            rq = qr[q].astype(np.float64) - Cr[j].astype(np.float64)
+            est, _ = orc.estimate_fullq(codes[r_], rq, D, float(n_o[r_]), float(rho[r_]))
+            assert abs(est - mth) <= band + 1e-6 * abs(mth), (q, x, est, mth, band)
+    ri, rd = orc.rerank(Q.numpy(), X.numpy(), gt, k)
+    pu.check_final(ids, d, ri, rd, k)
+
+
 def test_cfg1_end_to_end(orc):
     """CFG1 at full size (N = 1e5, D = 128, nlist 256, 100 queries, nprobe 16,
     k 10, M 100): GPU vs the oracle running the whole path independently (its

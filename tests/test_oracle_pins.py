@@ -624,3 +624,25 @@ def test_adaptive_rerank_recall(orc):
     nr2 = np.empty(40, np.int64)
     idx.search(Q, k, nprobe, M, rerank_mode=1, eps0=0.5, n_reranked=nr2)
     assert np.all(nr2 <= nr)
+
+
+# ------------------------------------------- qmode 1, NEXT-1
+def test_fullq_search_exhaustive_and_more_accurate(orc):
+    """The unquantized-query search (qmode 1): exhaustive probing with M >= N is
+    exact kNN (numpy); its estimates of the true squared distances have a
+    smaller error than the 4-bit query's (no query SQ is more precise)."""
+    X, Q = _mixture(43, 1200, 64, 8, 10)
+    idx = orc.OracleIndex(X, 8, seed=7, max_iter=8)
+    ids, d = idx.search(Q, 5, 8, 1200, qmode=1)
+    rid, rd = _np_knn(X, Q, 5)
+    assert np.array_equal(ids, rid) and np.allclose(d, rd.astype(np.float32), rtol=1e-6)
+    err = {}
+    for qm in (0, 1):
+        _, _, _, tids, test = idx.search(Q, 5, 8, 1200, qmode=qm, debug=True)
+        e = []
+        for q in range(10):
+            v = tids[q] >= 0
+            true = ((X[tids[q][v]].astype(np.float64) - Q[q].astype(np.float64)) ** 2).sum(1)
+            e.append(np.abs(test[q][v] - true))
+        err[qm] = np.concatenate(e).mean()
+    assert err[1] < err[0], err
