@@ -68,10 +68,10 @@ constexpr int kMinAStages = 3;
 // queries per group: all K chunks of a group fit the resident B region, and
 // the double-buffered accumulator leaves TMEM room for >= 2 A slots (ta: B
 // resident + >= 3 A stages + column constants fit shared memory; N <= 256)
-__host__ __device__ inline int group_cols(int Dp, bool ta) {
+__host__ __device__ inline int group_cols(int Dp, bool ta, int ngmax = kTN) {
     const int nch = (Dp + kKC - 1) / kKC;
     if (ta) {
-        int n = kTN;
+        int n = ngmax;
         while (n > kBoxRows && nch * n * kKC + kMinAStages * kAStage + 2 * n * (int)sizeof(ColC) + 2048 > kSmemLimit)
             n -= kBoxRows;
         return n;
@@ -86,10 +86,10 @@ struct SmemPlan {
     int nchunks, NG, slots;
     uint32_t acc_cols, off_colc, off_raw, total;
 };
-__host__ __device__ inline SmemPlan smem_plan(int Dp, bool ta) {
+__host__ __device__ inline SmemPlan smem_plan(int Dp, bool ta, int ngmax = kTN) {
     SmemPlan p;
     p.nchunks = (Dp + kKC - 1) / kKC;
-    p.NG = group_cols(Dp, ta);
+    p.NG = group_cols(Dp, ta, ngmax);
     p.acc_cols = (uint32_t)((p.NG + 31) & ~31);  // per accumulator buffer
     const uint32_t bres = (uint32_t)(p.nchunks * p.NG * kKC);
     p.off_colc = bres;  // [2][NG / 2] ColPair
@@ -281,7 +281,7 @@ __global__ __launch_bounds__(n_threads(kTA), 1) void scan_imma_kernel(const __gr
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
     uint8_t* smem = smem_raw + pad;
-    const SmemPlan sp = smem_plan(a.Dp, kTA);
+    const SmemPlan sp = smem_plan(a.Dp, kTA, a.ngmax);
     uint8_t* Bres = smem;                                        // [nchunks][NG rows][128 B], 128-byte swizzle
     ColPair* colc = reinterpret_cast<ColPair*>(smem + sp.off_colc);  // [2][NG / 2]
     __shared__ __align__(8) uint64_t full_bar[kMaxSlots], empty_bar[kMaxSlots], accf_bar[2], acce_bar[2],
@@ -781,6 +781,14 @@ __global__ void expand_codes_kernel(const uint32_t* __restrict__ codes, int64_t 
 
 }  // namespace
 
+// largest group (B columns) of the TMA-A scan: fewer columns leave shared memory
+// for more A stages in flight (diagnostics: RABITQ_TA_NGMAX, multiple of 32)
+int ta_ngmax() {
+    const char* env = getenv("RABITQ_TA_NGMAX");
+    const int v = env ? atoi(env) : kTN;
+    return std::max(kBoxRows, std::min(kTN, v / kBoxRows * kBoxRows));
+}
+
 const uint8_t* codes8_of(const rabitq_index* idx) {
     const char* env = getenv("RABITQ_CODES8");  // "0": expand in the kernel (diagnostics / tests)
     return (env && env[0] == '0') ? nullptr : idx->codes8;
@@ -831,7 +839,7 @@ void prepare_groups(const rabitq_index* idx, const int32_t* probes, int64_t n, c
     group_fill_kernel<<<grid, 256, 0, st>>>(probes, sub, n, g.gstart.p, g.gfill.p, g.gpos.p, g.gpair.p, rows);
     RQ_CHECK_LAUNCH();
     list_items_kernel<<<(nlist + 256) / 256, 256, 0, st>>>(nlist, idx->list_off, g.gcount.p,
-                                                           group_cols(g.Dp, codes8_of(idx) != nullptr),
+                                                           group_cols(g.Dp, codes8_of(idx) != nullptr, ta_ngmax()),
                                                            g.itemc.p);
     RQ_CHECK_LAUNCH();
     RQ_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb2, g.itemc.p, g.list_items.p, nlist + 1, st));
@@ -844,7 +852,7 @@ void group_items(const rabitq_index* idx, const int64_t* list_off, const Groups&
     itemc.alloc((size_t)nlist + 1, st);
     items.alloc((size_t)nlist + 1, st);
     list_items_kernel<<<(nlist + 256) / 256, 256, 0, st>>>(nlist, list_off, g.gcount.p,
-                                                           group_cols(g.Dp, codes8_of(idx) != nullptr), itemc.p);
+                                                           group_cols(g.Dp, codes8_of(idx) != nullptr, ta_ngmax()), itemc.p);
     RQ_CHECK_LAUNCH();
     size_t tb = 0;
     RQ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, itemc.p, items.p, nlist + 1, st));
@@ -924,7 +932,8 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         RQ_REQUIRE(cr == CUDA_SUCCESS, RABITQ_ERR_CUDA, "cuTensorMapEncodeTiled (A) failed: " + std::to_string((int)cr));
     }
-    const SmemPlan plan = smem_plan(a.Dp, ta);
+    a.ngmax = ta_ngmax();
+    const SmemPlan plan = smem_plan(a.Dp, ta, a.ngmax);
     RQ_REQUIRE(plan.slots >= 2 && plan.total <= (uint32_t)kSmemLimit, RABITQ_ERR_INTERNAL,
                "grouped scan: TMEM / shared-memory plan does not fit");
     const size_t smem = plan.total;

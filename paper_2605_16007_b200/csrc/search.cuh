@@ -59,6 +59,7 @@ struct ScanArgs {
     const int64_t* dense_base;  // [nq] first key of each query
     const int64_t* dense_off;   // [npairs] offset of each (query, probe) pair within its query
     int full;                   // 1: unquantized query (NEXT-1), 4 digit rows per pair (npairs = rows)
+    int ngmax;                  // TMA-A scan: largest group (set by scan_imma)
 };
 
 template <typename T>
@@ -92,6 +93,7 @@ bool imma_wanted(const rabitq_index* idx, int64_t npairs, int scan_path);
 void expand_codes(rabitq_index* idx, cudaStream_t st);
 // the expanded codes the grouped scan uses (nullptr: in-kernel expansion)
 const uint8_t* codes8_of(const rabitq_index* idx);
+int ta_ngmax();
 
 struct RerankArgs {
     const int* cnt;
