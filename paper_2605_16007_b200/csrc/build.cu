@@ -304,6 +304,8 @@ void free_index_memory(rabitq_index* idx) {
     idx->Xs = nullptr;
     cudaFree(idx->codes8);
     idx->codes8 = nullptr;
+    if (idx->side) cudaStreamDestroy(idx->side);
+    idx->side = nullptr;
     cudaFree(idx->Corig);
     idx->Corig = nullptr;
     cudaFree(idx->list_amax);

@@ -15,6 +15,7 @@
 struct rabitq_index {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;   // search: the re-rank ordering + dense block overlap the scan on it
     int D = 0, W = 0, nlist = 0;
     int64_t n = 0, id_offset = 0, nslots = 0, max_list = 0;
     uint64_t seed = 0;

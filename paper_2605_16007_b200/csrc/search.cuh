@@ -94,6 +94,7 @@ void expand_codes(rabitq_index* idx, cudaStream_t st);
 // the expanded codes the grouped scan uses (nullptr: in-kernel expansion)
 const uint8_t* codes8_of(const rabitq_index* idx);
 int ta_ngmax();
+cudaStream_t side_stream(const rabitq_index* idx);
 
 struct RerankArgs {
     const int* cnt;
@@ -130,6 +131,13 @@ struct RerankArgs {
     // bound-driven re-rank set (NEXT-4): keep est - bound <= k-th smallest est + bound
     int adaptive;
     unsigned long long* reranked;  // [1] candidates kept, summed over queries (adaptive only)
+    // split re-rank (select_rerank_kernel<2> + rr_gather / rr_filter / rr_final):
+    // per (query, candidate i) scratch at q Mp + i and the exact-distance task list
+    uint64_t* dk_g;                // [nq x Mp] (d or d~ + delta, row) keys
+    float* lowb_g;                 // [nq x Mp] d~ - delta (dense candidates), +inf otherwise
+    int* m_g;                      // [nq] candidates of each query
+    uint2* tasks;                  // {q Mp + i, row}
+    unsigned int* ntask;           // [1]
 };
 
 struct SearchCfg {

@@ -347,6 +347,24 @@ def test_fullq_parity(orc, D, N, nlist, nq, nprobe, k, M):
     pu.check_final(ids, d, ri, rd, k)
 
 
+@pytest.mark.parametrize("D", [128, 960])
+def test_split_rerank_identical(D, monkeypatch):
+    """The split re-rank path (select -> persistent gather -> dense filter ->
+    gather -> top-k, RABITQ_RR_SPLIT=1) returns exactly the fused kernel's ids
+    and distances (same candidates, same exact-distance arithmetic), with and
+    without the dense nearest-list block (>= 256 queries)."""
+    X, Q = make_data(D, 40000 if D < 900 else 8000, 32, 300)
+    idx = build(X, 32)
+    a_i, a_d = idx.search(Q.cuda(), 10, 8, 200)
+    monkeypatch.setenv("RABITQ_RR_SPLIT", "1")
+    b_i, b_d = idx.search(Q.cuda(), 10, 8, 200)
+    c_i, c_d = idx.search(Q[:100].cuda(), 10, 8, 200)  # < 256 queries: no dense block
+    monkeypatch.delenv("RABITQ_RR_SPLIT")
+    e_i, e_d = idx.search(Q[:100].cuda(), 10, 8, 200)
+    assert torch.equal(a_i, b_i) and torch.equal(a_d, b_d)
+    assert torch.equal(c_i, e_i) and torch.equal(c_d, e_d)
+
+
 def test_cfg1_end_to_end(orc):
     """CFG1 at full size (N = 1e5, D = 128, nlist 256, 100 queries, nprobe 16,
     k 10, M 100): GPU vs the oracle running the whole path independently (its
