@@ -92,3 +92,32 @@ def test_argument_errors_without_gpu(lib):
     h = ctypes.c_void_p()
     assert lib.rabitq_search(None, None, 0, 1, 1, 1, None, None) == rq.ERR_INVALID_ARGUMENT
     lib.rabitq_free(None)  # no-op
+
+
+def _struct_fields(name):
+    """Member names, in order, of `typedef struct { ... } name;` in include/rabitq.h."""
+    src = open(os.path.join(ROOT, "include", "rabitq.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    m = re.search(r"typedef struct \{([^{}]*)\}\s*" + re.escape(name) + r"\s*;", src)
+    assert m, name
+    names = []
+    for decl in m.group(1).split(";"):
+        decl = decl.strip()
+        if not decl:
+            continue
+        head, _, rest = decl.partition(" ")
+        for part in rest.split(","):
+            part = part.strip().lstrip("*").strip()
+            names.append(re.sub(r"\[.*\]", "", part).strip())
+    return names
+
+
+@pytest.mark.parametrize("cname,pyname", [("rabitq_search_opts", "SearchOpts"), ("rabitq_profile", "Profile"),
+                                          ("rabitq_index_info_t", "IndexInfo")])
+def test_binding_structs_match_header(cname, pyname):
+    """The ctypes mirrors of the C-ABI structs list the header's members in the
+    header's order (an appended field on one side only would shift the rest)."""
+    import paper_2605_16007_b200 as rq
+
+    py = [f for f, _ in getattr(rq, pyname)._fields_]
+    assert py == _struct_fields(cname), (py, _struct_fields(cname))
