@@ -663,6 +663,232 @@ __global__ __launch_bounds__(n_threads(kTA), 1) void scan_imma_kernel(const __gr
     if (warp == kMmaWarp) tc::tmem_dealloc(tmem, kTmemCols);
 }
 
+// ------------------------------------------------- operand-swapped main scan
+// The main scan (rank key EST, no dump / re-scan / dense mode, 4-bit query)
+// with the roles of the operands swapped: the group's <= 128 quantized queries
+// are the A operand, resident in TMEM for a whole item (K = Dp bytes = Dp / 4
+// columns), and each 128-vector code tile is the B operand, streamed from the
+// expanded codes by TMA through kSwB shared-memory stages.  D[query][vector]
+// sits in TMEM with one query per lane, so the epilogue keeps the query's
+// column constants in registers and reserves a lane's survivors of a 16-vector
+// chunk with one counter atomic.  Same arithmetic per (query, vector) as
+// scan_imma_kernel: identical keys and survivors.
+constexpr int kSwNG = 128;        // queries per group (UMMA M)
+constexpr int kSwB = 12;          // code stages (16 KB each)
+constexpr int kSwEpi0 = 6;        // warps 0 loader, 1 MMA, 2-5 query writers, 6-21 epilogue
+constexpr int kSwNT = (kSwEpi0 + kEpiWarps) * 32;
+constexpr int kSwAcc = 128;       // accumulator columns per buffer (128 vectors)
+__global__ __launch_bounds__(kSwNT, 1) void scan_swap_kernel(const __grid_constant__ CUtensorMap tmapC, ScanArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
+    uint8_t* stages = smem_raw + pad;  // [kSwB][128 vectors][128 bytes], 128-byte swizzle
+    __shared__ __align__(8) uint64_t full_bar[kSwB], empty_bar[kSwB], accf_bar[2], acce_bar[2],
+        afull_bar[kMaxChunks], afree_bar[kMaxChunks], vfull_bar[2];
+    __shared__ __align__(16) float4 vconst[2][kTM / 2];  // per tile buffer: (f0, A0, f1, A1) per vector pair
+    __shared__ __align__(16) float2 vpc[2][kTM / 2];     // (pcf0, pcf1)
+    __shared__ uint32_t vrow[2][kTM];
+    __shared__ uint32_t tmem_base_s;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nchunks = (a.Dp + kKC - 1) / kKC;
+    if (warp == 1) tc::tmem_alloc(&tmem_base_s, kTmemCols);
+    if (tid == 0) {
+        for (int s = 0; s < kSwB; ++s) {
+            tc::mbar_init(&full_bar[s], 1);
+            tc::mbar_init(&empty_bar[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&accf_bar[b], 1);
+            tc::mbar_init(&acce_bar[b], kEpiWarps);
+        }
+        for (int c = 0; c < kMaxChunks; ++c) {
+            tc::mbar_init(&afull_bar[c], 4);  // one arrive per query-writer warp
+            tc::mbar_init(&afree_bar[c], 1);
+        }
+        tc::prefetch_tmap(&tmapC);
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = tmem_base_s;
+    const uint32_t tmemA = tmem + 2u * kSwAcc;  // the queries: Dp / 4 columns
+    const int64_t total = a.list_items[a.nlist];
+
+    if (warp == 0) {
+        // ================= code tiles (B) by TMA =================
+        if (lane == 0) {
+            uint32_t gc = 0;
+            for (int64_t item = blockIdx.x; item < total; item += gridDim.x) {
+                const Item it = decode_item(a, kSwNG, item);
+                for (int t = 0; t < it.ntiles; ++t) {
+                    const int row0 = (int)(it.slot_base + (it.t0 + t) * kTM);
+                    for (int c = 0; c < nchunks; ++c, ++gc) {
+                        const int s = (int)(gc % kSwB);
+                        const uint32_t u = gc / kSwB;
+                        if (u > 0) tc::mbar_wait_backoff(&empty_bar[s], (u - 1) & 1);
+                        tc::mbar_arrive_expect_tx(&full_bar[s], (uint32_t)kAStage);
+                        tc::tma_load_2d(stages + s * kAStage, &tmapC, &full_bar[s], c * kKC, row0);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ================= MMA issuer =================
+        uint32_t gc = 0, tcnt = 0, ic = 0;
+        const uint32_t idesc = tc::idesc_i8(kSwNG, kTM, /*a_signed=*/false, /*b_signed=*/true);
+        for (int64_t item = blockIdx.x; item < total; item += gridDim.x, ++ic) {
+            const Item it = decode_item(a, kSwNG, item);
+            for (int t = 0; t < it.ntiles; ++t, ++tcnt) {
+                const int b = tcnt & 1;
+                const uint32_t ub = tcnt >> 1;
+                if (ub > 0) tc::mbar_wait_backoff(&acce_bar[b], (ub - 1) & 1);
+                tc::fence_after_sync();
+                const uint32_t dacc = tmem + (uint32_t)b * kSwAcc;
+                for (int c = 0; c < nchunks; ++c, ++gc) {
+                    const int s = (int)(gc % kSwB);
+                    const int nks = min(kKC, a.Dp - c * kKC) / 32;
+                    if (t == 0) tc::mbar_wait(&afull_bar[c], ic & 1);  // the item's query chunk c is in TMEM
+                    tc::mbar_wait(&full_bar[s], (gc / kSwB) & 1);
+                    tc::fence_after_sync();
+                    const uint64_t bd = tc::smem_desc_sw128(tc::smem_u32(stages + s * kAStage));
+                    tc::mma_i8_ts_chunk(dacc, tmemA + (uint32_t)(c * kChunkCols), bd, idesc, c > 0 ? 1u : 0u, nks,
+                                        &empty_bar[s]);
+                    if (t == it.ntiles - 1) tc::commit_warp(&afree_bar[c]);  // query chunk c free for the next item
+                    if (c == nchunks - 1) tc::commit_warp(&accf_bar[b]);
+                }
+            }
+        }
+    } else if (warp < kSwEpi0) {
+        // ================= queries (A) into TMEM =================
+        const int qq = warp & 3;              // TMEM lane quarter of this warp
+        const int r = qq * 32 + lane;         // query row of the group = TMEM lane
+        const uint32_t lane_addr = (uint32_t)(qq * 32) << 16;
+        uint32_t ic = 0;
+        for (int64_t item = blockIdx.x; item < total; item += gridDim.x, ++ic) {
+            const Item it = decode_item(a, kSwNG, item);
+            const uint4* src = reinterpret_cast<const uint4*>(a.qbar8 + (size_t)(it.grow0 + r) * a.Dp);
+            const bool ok = r < it.ncols;
+            for (int c = 0; c < nchunks; ++c) {
+                // chunk c (128 K bytes = 32 columns) once the previous item's last tile used it
+                uint4 v[8];
+                const int nq4 = min(kKC, a.Dp - c * kKC) / 16;  // 16-byte words in this chunk (4 or 8)
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    v[k] = (ok && k < nq4) ? __ldg(src + c * 8 + k) : make_uint4(0u, 0u, 0u, 0u);
+                if (ic > 0) tc::mbar_wait_backoff(&afree_bar[c], (ic - 1) & 1);
+                tc::fence_after_sync();
+                const uint32_t dst = tmemA + lane_addr + (uint32_t)(c * kChunkCols);
+                tc::tmem_st16(dst, v[0], v[1], v[2], v[3]);
+                if (nq4 > 4) tc::tmem_st16(dst + 16, v[4], v[5], v[6], v[7]);
+                tc::tmem_st_wait();
+                tc::fence_before_sync();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&afull_bar[c]);
+            }
+        }
+    } else {
+        // ================= epilogue: lane = query, columns = vectors =================
+        const int e = warp - kSwEpi0;
+        const int quarter = warp & 3;
+        const int part = e >> 2;              // column chunks part, part + 4 (16 vectors each)
+        const int r = quarter * 32 + lane;    // query row of the group
+        uint32_t tcnt = 0;
+        for (int64_t item = blockIdx.x; item < total; item += gridDim.x) {
+            const Item it = decode_item(a, kSwNG, item);
+            const bool qok = r < it.ncols;
+            ColC cc;
+            if (qok) {
+                cc = a.gcolc[it.grow0 + r];
+            } else {
+                cc.a = cc.b = cc.K = cc.nq2 = 0.f;
+                cc.tau = cc.U = -INFINITY;
+                cc.q = 0;
+                cc.pair = -1;
+            }
+            const float2 nb_pc = make_float2(cc.b, cc.b), nK2 = make_float2(-cc.K, -cc.K);
+            const float2 na2 = make_float2(-cc.a, -cc.a), mg2 = make_float2(12582912.0f, 12582912.0f);
+            for (int t = 0; t < it.ntiles; ++t, ++tcnt) {
+                const int b = tcnt & 1;
+                const uint32_t ub = tcnt >> 1;
+                const int64_t vbase = (it.t0 + t) * kTM;
+                {
+                    // the tile's vector constants in shared memory (double-buffered by tile
+                    // parity; the barrier below also ends every warp's use of this buffer
+                    // two tiles ago): (-f0, -f1, A0, A1), (pcf0, pcf1), rows
+                    const int et = e * 32 + lane;
+                    if (et < kTM / 2) {
+                        const int64_t v0 = vbase + 2 * et;
+                        const bool ok0 = v0 < it.L, ok1 = v0 + 1 < it.L;
+                        const float2 f0 = ok0 ? __ldg(a.fac + it.slot_base + v0) : make_float2(0.f, 0.f);
+                        const float2 f1 = ok1 ? __ldg(a.fac + it.slot_base + v0 + 1) : make_float2(0.f, 0.f);
+                        vconst[b][et] = make_float4(-f0.y, -f1.y, f0.x, f1.x);
+                        vpc[b][et] = make_float2(ok0 ? (float)__ldg(a.pcnt + it.slot_base + v0) : 0.f,
+                                                 ok1 ? (float)__ldg(a.pcnt + it.slot_base + v0 + 1) : 0.f);
+                    } else if (et < kTM / 2 + kTM) {
+                        const int64_t v = vbase + (et - kTM / 2);
+                        vrow[b][et - kTM / 2] = v < it.L ? __ldg(a.rows + it.slot_base + v) : 0u;
+                    }
+                    tc::named_barrier(1, kEpiWarps * 32);
+                }
+                tc::mbar_wait(&accf_bar[b], ub & 1);
+                tc::fence_after_sync();
+                uint32_t hc_bits[2];
+                int hc_base[2];
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const int col0 = (part + 4 * k) * 16;
+                    const uint32_t tcol = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)b * kSwAcc + col0;
+                    uint32_t acc[16];
+                    tc::tmem_ld16(tcol, acc);
+                    uint32_t bits = 0u;
+                    const int64_t nval = it.L - (vbase + col0);  // valid vectors from col0 on
+#pragma unroll
+                    for (int i = 0; i < 16; i += 2) {
+                        const float4 vc = vconst[b][(col0 + i) >> 1];
+                        const float2 pc = vpc[b][(col0 + i) >> 1];
+                        const float2 ipn = fsub2(make_float2(__int_as_float(0x4B400000 + (int)acc[i]),
+                                                             __int_as_float(0x4B400000 + (int)acc[i + 1])), mg2);
+                        const float2 inner = ffma2(nb_pc, pc, nK2);
+                        const float2 tt = ffma2(na2, ipn, inner);
+                        const float2 vv = ffma2(make_float2(vc.x, vc.y), tt, make_float2(vc.z, vc.w));
+                        bits |= (vv.x <= cc.U ? 1u : 0u) << i;
+                        bits |= (vv.y <= cc.U ? 1u : 0u) << (i + 1);
+                    }
+                    if (nval < 16) bits &= nval > 0 ? (1u << nval) - 1u : 0u;
+                    if (!qok) bits = 0u;
+                    hc_bits[k] = bits;
+                    hc_base[k] = bits ? atomicAdd(&a.cnt[cc.q], __popc(bits)) : 0;
+                }
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const uint32_t bits = hc_bits[k];
+                    uint32_t cols = __reduce_or_sync(0xFFFFFFFFu, bits);
+                    const int col0 = (part + 4 * k) * 16;
+                    const uint32_t tcol = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)b * kSwAcc + col0;
+                    for (; cols; cols &= cols - 1) {
+                        const int i = __ffs(cols) - 1;
+                        const uint32_t acci = tc::tmem_ld1(tcol + (uint32_t)i);
+                        if ((bits >> i) & 1u) {
+                            const int c = col0 + i;
+                            const float4 vc = vconst[b][c >> 1];
+                            const float2 pc = vpc[b][c >> 1];
+                            const float2 fac = (c & 1) ? make_float2(vc.w, -vc.y) : make_float2(vc.z, -vc.x);
+                            const float key = est_of(acci, cc, fac, (c & 1) ? pc.y : pc.x);
+                            const int pos = hc_base[k] + __popc(bits & ((1u << i) - 1u));
+                            if (pos < a.cap) a.buf[(size_t)cc.q * a.cap + pos] = make_key(key, vrow[b][c]);
+                        }
+                    }
+                }
+                tc::fence_before_sync();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&acce_bar[b]);
+            }
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 1) tc::tmem_dealloc(tmem, kTmemCols);
+}
+
 // ------------------------------------------------------------ list grouping
 // pairs to group: all (sub == nullptr) or the listed pair indices
 // rows = grouped B rows per pair (1; 4 for the unquantized query's digit rows)
@@ -776,6 +1002,20 @@ __global__ void expand_codes_kernel(const uint32_t* __restrict__ codes, int64_t 
         if (s < nslots) expand32(__ldg(codes + ((s >> 5) * W + w) * 32 + (s & 31)), lo, hi);
         out[2 * e] = lo;
         out[2 * e + 1] = hi;
+    }
+}
+
+__global__ void list_items_gstart_kernel(int nlist, const int64_t* __restrict__ list_off,
+                                         const int64_t* __restrict__ gstart, int NG, int64_t* __restrict__ items) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= nlist; j += gridDim.x * blockDim.x) {
+        if (j == nlist) {
+            items[j] = 0;
+            continue;
+        }
+        const int64_t L = list_off[j + 1] - list_off[j];
+        const int64_t G = gstart[j + 1] - gstart[j];
+        const int64_t ntl = (L + kTM - 1) / kTM;
+        items[j] = ((ntl + kTilesPerItem - 1) / kTilesPerItem) * ((G + NG - 1) / NG);
     }
 }
 
@@ -933,6 +1173,33 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
         RQ_REQUIRE(cr == CUDA_SUCCESS, RABITQ_ERR_CUDA, "cuTensorMapEncodeTiled (A) failed: " + std::to_string((int)cr));
     }
     a.ngmax = ta_ngmax();
+    // operand-swapped main scan (queries resident in TMEM, code tiles streamed
+    // through 12 stages): opt-in (RABITQ_SWAP=1), bit-identical but slower as
+    // built (CFG2 scan 4.47 vs 3.66 ms, CFG3 7.37 vs 4.86 ms): groups of 128
+    // queries (TMEM holds the queries and both 128-column accumulators) mean
+    // more tile passes than the 160 / 256-column groups of scan_imma_kernel
+    const char* sw_env = getenv("RABITQ_SWAP");
+    if (ta && !lb && !dump && !retry && !dense && !a.full && sw_env && sw_env[0] == '1' && a.experiment == 0 &&
+        a.Dp <= 1024) {
+        WBuf<int64_t> itemc, items;
+        itemc.alloc((size_t)a.nlist + 1, st);
+        items.alloc((size_t)a.nlist + 1, st);
+        list_items_gstart_kernel<<<(a.nlist + 256) / 256, 256, 0, st>>>(a.nlist, a.list_off, a.gstart, kSwNG,
+                                                                       itemc.p);
+        RQ_CHECK_LAUNCH();
+        size_t tb = 0;
+        RQ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, itemc.p, items.p, a.nlist + 1, st));
+        WBuf<uint8_t> tmp;
+        tmp.alloc(tb, st);
+        RQ_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, itemc.p, items.p, a.nlist + 1, st));
+        ScanArgs s = a;
+        s.list_items = items.p;
+        const size_t smem = (size_t)kSwB * kAStage + 1024;
+        RQ_CUDA(cudaFuncSetAttribute(scan_swap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        scan_swap_kernel<<<sms, kSwNT, smem, st>>>(tmapA, s);
+        RQ_CHECK_LAUNCH();
+        return;
+    }
     const SmemPlan plan = smem_plan(a.Dp, ta, a.ngmax);
     RQ_REQUIRE(plan.slots >= 2 && plan.total <= (uint32_t)kSmemLimit, RABITQ_ERR_INTERNAL,
                "grouped scan: TMEM / shared-memory plan does not fit");

@@ -150,10 +150,10 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
 }
 
 // Instruction descriptor, .kind::i8: D = s32, A = u8 or s8, B = u8, both K-major.
-__host__ __device__ constexpr uint32_t idesc_i8(int M, int N, bool a_signed = false) {
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N, bool a_signed = false, bool b_signed = false) {
     return (2u << 4)                       // c_format: S32
            | ((a_signed ? 1u : 0u) << 7)   // a format: 0 unsigned / 1 signed 8-bit
-           | (0u << 10)                    // b format: unsigned 8-bit
+           | ((b_signed ? 1u : 0u) << 10)  // b format: 0 unsigned / 1 signed 8-bit
            | (0u << 15) | (0u << 16)       // a/b major: K
            | ((uint32_t)(N >> 3) << 17)    // N / 8
            | ((uint32_t)(M >> 4) << 24);   // M / 16
@@ -275,6 +275,16 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint4& lo, const 
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(lo.x),
                  "r"(lo.y), "r"(lo.z), "r"(lo.w), "r"(hi.x), "r"(hi.y), "r"(hi.z), "r"(hi.w)
                  : "memory");
+}
+// 32 lanes x 16 columns of 32-bit into TMEM
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint4& a, const uint4& b, const uint4& c,
+                                          const uint4& d) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w), "r"(c.x), "r"(c.y), "r"(c.z),
+        "r"(c.w), "r"(d.x), "r"(d.y), "r"(d.z), "r"(d.w)
+        : "memory");
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 

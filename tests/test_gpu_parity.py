@@ -365,6 +365,18 @@ def test_split_rerank_identical(D, monkeypatch):
     assert torch.equal(c_i, e_i) and torch.equal(c_d, e_d)
 
 
+@pytest.mark.parametrize("D", [96, 960])
+def test_swapped_scan_identical(D, monkeypatch):
+    """The operand-swapped main scan (RABITQ_SWAP=1: queries resident in TMEM,
+    code tiles streamed) returns exactly the default kernel's results."""
+    X, Q = make_data(D, 40000 if D < 900 else 8000, 32, 300)
+    idx = build(X, 32)
+    a_i, a_d = idx.search(Q.cuda(), 10, 8, 200, scan_path=rq.SCAN_IMMA)
+    monkeypatch.setenv("RABITQ_SWAP", "1")
+    b_i, b_d = idx.search(Q.cuda(), 10, 8, 200, scan_path=rq.SCAN_IMMA)
+    assert torch.equal(a_i, b_i) and torch.equal(a_d, b_d)
+
+
 def test_cfg1_end_to_end(orc):
     """CFG1 at full size (N = 1e5, D = 128, nlist 256, 100 queries, nprobe 16,
     k 10, M 100): GPU vs the oracle running the whole path independently (its
