@@ -47,7 +47,7 @@ constexpr int kMaxChunks = 8;              // Dp <= 1024
 constexpr int kMaxSlots = 8;               // A ring slots in TMEM
 constexpr int kBRes = 192 * 1024;          // resident query operand (all K chunks of one group)
 constexpr int kMaxNG = 224;                // 2 NG accumulator columns + >= 2 A slots <= 512
-constexpr int kBoxRows = 32;               // TMA box = 32 query rows x 128 bytes
+constexpr int kBoxRows = 16;               // TMA box = 16 query rows x 128 bytes (group width granularity)
 constexpr int kTilesPerItem = 8;           // vector tiles per work item (B loaded once per item)
 constexpr int kProdWarps = 4;              // thread r expands code row r into TMEM lane r
 constexpr int kMmaWarp = kProdWarps;       // warp 4 issues the UMMAs (and owns TMEM)
@@ -68,11 +68,11 @@ constexpr int kMinAStages = 3;
 // queries per group: all K chunks of a group fit the resident B region, and
 // the double-buffered accumulator leaves TMEM room for >= 2 A slots (ta: B
 // resident + >= 3 A stages + column constants fit shared memory; N <= 256)
-__host__ __device__ inline int group_cols(int Dp, bool ta, int ngmax = kTN) {
+__host__ __device__ inline int group_cols(int Dp, bool ta, int ngmax = kTN, int minst = kMinAStages) {
     const int nch = (Dp + kKC - 1) / kKC;
     if (ta) {
         int n = ngmax;
-        while (n > kBoxRows && nch * n * kKC + kMinAStages * kAStage + 2 * n * (int)sizeof(ColC) + 2048 > kSmemLimit)
+        while (n > kBoxRows && nch * n * kKC + minst * kAStage + 2 * n * (int)sizeof(ColC) + 2048 > kSmemLimit)
             n -= kBoxRows;
         return n;
     }
@@ -86,10 +86,10 @@ struct SmemPlan {
     int nchunks, NG, slots;
     uint32_t acc_cols, off_colc, off_raw, total;
 };
-__host__ __device__ inline SmemPlan smem_plan(int Dp, bool ta, int ngmax = kTN) {
+__host__ __device__ inline SmemPlan smem_plan(int Dp, bool ta, int ngmax = kTN, int minst = kMinAStages) {
     SmemPlan p;
     p.nchunks = (Dp + kKC - 1) / kKC;
-    p.NG = group_cols(Dp, ta, ngmax);
+    p.NG = group_cols(Dp, ta, ngmax, minst);
     p.acc_cols = (uint32_t)((p.NG + 31) & ~31);  // per accumulator buffer
     const uint32_t bres = (uint32_t)(p.nchunks * p.NG * kKC);
     p.off_colc = bres;  // [2][NG / 2] ColPair
@@ -281,7 +281,7 @@ __global__ __launch_bounds__(n_threads(kTA), 1) void scan_imma_kernel(const __gr
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
     uint8_t* smem = smem_raw + pad;
-    const SmemPlan sp = smem_plan(a.Dp, kTA, a.ngmax);
+    const SmemPlan sp = smem_plan(a.Dp, kTA, a.ngmax, a.minst);
     uint8_t* Bres = smem;                                        // [nchunks][NG rows][128 B], 128-byte swizzle
     ColPair* colc = reinterpret_cast<ColPair*>(smem + sp.off_colc);  // [2][NG / 2]
     __shared__ __align__(8) uint64_t full_bar[kMaxSlots], empty_bar[kMaxSlots], accf_bar[2], acce_bar[2],
@@ -1029,6 +1029,13 @@ int ta_ngmax() {
     return std::max(kBoxRows, std::min(kTN, v / kBoxRows * kBoxRows));
 }
 
+// fewest A stages of the TMA-A scan (the group shrinks to make room; 16-column steps)
+int ta_minstages() {
+    const char* env = getenv("RABITQ_TA_MINSTAGES");
+    const int v = env ? atoi(env) : kMinAStages;
+    return std::max(2, std::min(kMaxSlots, v));
+}
+
 const uint8_t* codes8_of(const rabitq_index* idx) {
     const char* env = getenv("RABITQ_CODES8");  // "0": expand in the kernel (diagnostics / tests)
     return (env && env[0] == '0') ? nullptr : idx->codes8;
@@ -1079,7 +1086,7 @@ void prepare_groups(const rabitq_index* idx, const int32_t* probes, int64_t n, c
     group_fill_kernel<<<grid, 256, 0, st>>>(probes, sub, n, g.gstart.p, g.gfill.p, g.gpos.p, g.gpair.p, rows);
     RQ_CHECK_LAUNCH();
     list_items_kernel<<<(nlist + 256) / 256, 256, 0, st>>>(nlist, idx->list_off, g.gcount.p,
-                                                           group_cols(g.Dp, codes8_of(idx) != nullptr, ta_ngmax()),
+                                                           group_cols(g.Dp, codes8_of(idx) != nullptr, ta_ngmax(), ta_minstages()),
                                                            g.itemc.p);
     RQ_CHECK_LAUNCH();
     RQ_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb2, g.itemc.p, g.list_items.p, nlist + 1, st));
@@ -1092,7 +1099,7 @@ void group_items(const rabitq_index* idx, const int64_t* list_off, const Groups&
     itemc.alloc((size_t)nlist + 1, st);
     items.alloc((size_t)nlist + 1, st);
     list_items_kernel<<<(nlist + 256) / 256, 256, 0, st>>>(nlist, list_off, g.gcount.p,
-                                                           group_cols(g.Dp, codes8_of(idx) != nullptr, ta_ngmax()), itemc.p);
+                                                           group_cols(g.Dp, codes8_of(idx) != nullptr, ta_ngmax(), ta_minstages()), itemc.p);
     RQ_CHECK_LAUNCH();
     size_t tb = 0;
     RQ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, itemc.p, items.p, nlist + 1, st));
@@ -1173,6 +1180,7 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
         RQ_REQUIRE(cr == CUDA_SUCCESS, RABITQ_ERR_CUDA, "cuTensorMapEncodeTiled (A) failed: " + std::to_string((int)cr));
     }
     a.ngmax = ta_ngmax();
+    a.minst = ta_minstages();
     // operand-swapped main scan (queries resident in TMEM, code tiles streamed
     // through 12 stages): opt-in (RABITQ_SWAP=1), bit-identical but slower as
     // built (CFG2 scan 4.47 vs 3.66 ms, CFG3 7.37 vs 4.86 ms): groups of 128
@@ -1200,7 +1208,7 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
         RQ_CHECK_LAUNCH();
         return;
     }
-    const SmemPlan plan = smem_plan(a.Dp, ta, a.ngmax);
+    const SmemPlan plan = smem_plan(a.Dp, ta, a.ngmax, a.minst);
     RQ_REQUIRE(plan.slots >= 2 && plan.total <= (uint32_t)kSmemLimit, RABITQ_ERR_INTERNAL,
                "grouped scan: TMEM / shared-memory plan does not fit");
     const size_t smem = plan.total;

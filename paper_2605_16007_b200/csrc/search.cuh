@@ -60,6 +60,7 @@ struct ScanArgs {
     const int64_t* dense_off;   // [npairs] offset of each (query, probe) pair within its query
     int full;                   // 1: unquantized query (NEXT-1), 4 digit rows per pair (npairs = rows)
     int ngmax;                  // TMA-A scan: largest group (set by scan_imma)
+    int minst;                  // TMA-A scan: fewest A stages (set by scan_imma)
 };
 
 template <typename T>
@@ -94,6 +95,7 @@ void expand_codes(rabitq_index* idx, cudaStream_t st);
 // the expanded codes the grouped scan uses (nullptr: in-kernel expansion)
 const uint8_t* codes8_of(const rabitq_index* idx);
 int ta_ngmax();
+int ta_minstages();
 cudaStream_t side_stream(const rabitq_index* idx);
 
 struct RerankArgs {
