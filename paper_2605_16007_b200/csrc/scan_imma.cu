@@ -1052,8 +1052,13 @@ bool imma_wanted(const rabitq_index* idx, int64_t npairs, int scan_path) {
     if (scan_path == RABITQ_SCAN_POPC) return false;
     if (idx->W > 4 * kMaxChunks) return false;  // B chunks (D <= 1024)
     if (scan_path == RABITQ_SCAN_IMMA) return true;
-    // AUTO: the tensor-core path pays once lists are shared by enough queries
-    return npairs >= (int64_t)8 * idx->nlist;
+    // AUTO: the tensor-core path pays once lists are shared by a few queries and
+    // the batch amortizes its fixed cost, and at any batch for long codes
+    // (measured, CFG2 D = 960: batch 64 0.75 vs 1.26 ms per search, 256: 1.12 vs
+    // 3.48; CFG3 D = 96: batch 64 popc 0.66 vs 1.12 ms, 256 (4 pairs per list):
+    // tensor cores 1.47 vs 1.95 ms; CFG1, 1600 pairs: popc 0.29 vs 0.42 ms)
+    return npairs >= (int64_t)8 * idx->nlist || (npairs >= (int64_t)4 * idx->nlist && npairs >= 8192) ||
+           idx->W >= 16;
 }
 
 void prepare_groups(const rabitq_index* idx, const int32_t* probes, int64_t n, const int32_t* sub, Groups& g,
