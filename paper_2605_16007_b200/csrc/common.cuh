@@ -171,6 +171,7 @@ __device__ __forceinline__ float rank_key(float est, float epsnq, float g1) {
 RQ_F2_OP(fadd2, "add.rn.f32x2")
 RQ_F2_OP(fsub2, "sub.rn.f32x2")
 RQ_F2_OP(fmul2, "mul.rn.f32x2")
+RQ_F2_OP(fadd2_rm, "add.rm.f32x2")  // round toward -inf
 #undef RQ_F2_OP
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
     float2 d;
