@@ -365,6 +365,17 @@ def test_split_rerank_identical(D, monkeypatch):
     assert torch.equal(c_i, e_i) and torch.equal(c_d, e_d)
 
 
+def test_scan_paths_identical_multigroup_d960():
+    """D = 960 with > 160 queries per list: several query groups per list (the
+    TMA-A kernel's 160-column groups) and several 8-tile items per group; the
+    tensor-core scan must still equal the popc scan bit for bit."""
+    X, Q = make_data(960, 24000, 8, 400)
+    idx = build(X, 8)
+    a_i, a_d = idx.search(Q.cuda(), 10, 4, 300, scan_path=rq.SCAN_POPC)
+    b_i, b_d = idx.search(Q.cuda(), 10, 4, 300, scan_path=rq.SCAN_IMMA)
+    assert torch.equal(a_i, b_i) and torch.equal(a_d, b_d)
+
+
 @pytest.mark.parametrize("D", [96, 960])
 def test_swapped_scan_identical(D, monkeypatch):
     """The operand-swapped main scan (RABITQ_SWAP=1: queries resident in TMEM,
