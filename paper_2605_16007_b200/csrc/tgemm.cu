@@ -392,7 +392,7 @@ __global__ __launch_bounds__(kNT, 1) void tgemm_kernel(const __grid_constant__ C
 // each fp32, so |d~ - d| <= 2^-8 (n_o^2 + ||q - c||^2) (the re-rank's filter
 // bound, search.cu).  Warp 0: TMA, warp 1: MMA, warps 2-5: epilogue.
 constexpr int kDK = 32;                       // floats of K per stage (128 bytes)
-constexpr int kDStages = 4;
+constexpr int kDStages = 2;  // 96 KB: leaves an SM room for quantizer blocks alongside (side-stream overlap)
 constexpr int kDA = kBM * kDK * 4;            // 16 KB
 constexpr int kDBoxRows = 64;                 // B box rows (n <= 256: up to 4 boxes)
 constexpr int kDB = kBN * kDK * 4;            // 32 KB (max)
