@@ -135,8 +135,12 @@ class ClockSampler:
 
 # ------------------------------------------------------------- workload --
 def workload(args):
-    s = synth.spec(args.config, **({"nq": args.nq} if args.nq else {}))
-    return s
+    ov = {}
+    if args.nq:
+        ov["nq"] = args.nq
+    if getattr(args, "nprobe", 0):
+        ov["nprobe"] = args.nprobe
+    return synth.spec(args.config, **ov)
 
 
 def build_shard(s, rank, world, dev, rq, proxy=None):
@@ -552,6 +556,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--nq", type=int, default=0, help="override the query count (quick runs)")
+    ap.add_argument("--nprobe", type=int, default=0, help="override nprobe (CFG3's sweep: 16/32/64/128)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--scan-path", type=int, default=0, dest="scan_path")
     ap.add_argument("--no-cpu-baseline", action="store_true")
