@@ -159,7 +159,18 @@ typedef struct {
                                 takes <x-bar, r_q> from r_q in 24-bit fixed point (error <= 1e-6
                                 n_o n_q), no Philox draws; grouped tensor-core scan only (d <= 1024,
                                 scan_path AUTO or IMMA), UNSUPPORTED otherwise */
+    uint32_t variant;        /* 0 (default) or an OR of RABITQ_VARIANT_*: alternative execution
+                                paths of the same computation (parity tests prove them
+                                bit-identical to the default); never changes results        */
 } rabitq_search_opts;
+
+/* rabitq_search_opts.variant bits (results are identical with any of them) */
+#define RABITQ_VARIANT_RADIX_PROBE 1u        /* probe top-nprobe by the radix select only        */
+#define RABITQ_VARIANT_EXPAND_IN_KERNEL 2u   /* grouped scan expands the codes into TMEM itself
+                                                 (ignores the index's expanded-code copy)        */
+#define RABITQ_VARIANT_NO_DENSE_RERANK 4u    /* exact gather of every re-rank candidate          */
+#define RABITQ_VARIANT_GENERIC_SCAN 8u       /* d <= 128: the generic grouped scan kernel instead
+                                                 of the small-K one                              */
 
 /* Search nq queries Q [nq x d] fp32: rotate, probe the nprobe
  * nearest lists, 4-bit Philox-randomized query quantization per (q, list),

@@ -23,6 +23,8 @@ LIB_PATH = os.path.join(_HERE, "librabitq.so")
 OK, ERR_INVALID_ARGUMENT, ERR_INVALID_DATA, ERR_OUT_OF_MEMORY, ERR_CUDA, ERR_NCCL, ERR_UNSUPPORTED, ERR_INTERNAL = range(8)
 SCAN_AUTO, SCAN_POPC, SCAN_IMMA = 0, 1, 2
 RANK_EST, RANK_LOWER_BOUND = 0, 1
+# rabitq_search_opts.variant bits: alternative execution paths, identical results
+VARIANT_RADIX_PROBE, VARIANT_EXPAND_IN_KERNEL, VARIANT_NO_DENSE_RERANK, VARIANT_GENERIC_SCAN = 1, 2, 4, 8
 RERANK_FIXED, RERANK_BOUND = 0, 1
 
 
@@ -100,6 +102,7 @@ class SearchOpts(ctypes.Structure):
         ("profile", ctypes.POINTER(Profile)),
         ("rerank", ctypes.c_int32),
         ("query_bits", ctypes.c_int32),
+        ("variant", ctypes.c_uint32),
     ]
 
 
@@ -180,6 +183,26 @@ def _stream_handle(stream) -> Optional[int]:
     return int(getattr(stream, "cuda_stream", stream))
 
 
+def _call_stream(stream, dev_tensor, temps):
+    """The stream a device-side call runs on: the caller's, else torch's
+    current stream on the tensor's device (so the library's kernels are
+    ordered after the torch work that produced the inputs).  Tensors created
+    here for the call (dtype / layout copies, outputs) are recorded on a
+    foreign stream so the caching allocator does not reuse them early."""
+    torch = _torch()
+    if dev_tensor is None or not dev_tensor.is_cuda:
+        return _stream_handle(stream)
+    if stream is None:
+        return torch.cuda.current_stream(dev_tensor.device).cuda_stream
+    h = _stream_handle(stream)
+    if h != torch.cuda.current_stream(dev_tensor.device).cuda_stream:
+        ext = stream if isinstance(stream, torch.cuda.Stream) else torch.cuda.ExternalStream(h, device=dev_tensor.device)
+        for t in temps:
+            if t is not None and t.is_cuda:
+                t.record_stream(ext)
+    return h
+
+
 class Index:
     """An IVF-RaBitQ index on one GPU (``rabitq_build_ex``)."""
 
@@ -208,6 +231,8 @@ class Index:
         o.borrow_vectors = 1 if borrow else 0
         o.id_offset = id_offset
         o.device = device if device >= 0 else (X.device.index if X.is_cuda else -1)
+        if X.is_cuda:  # the build runs on its own stream: inputs produced by torch must be complete
+            _torch().cuda.current_stream(X.device).synchronize()
         h = ctypes.c_void_p()
         _check(lib().rabitq_build_ex(ctypes.c_void_p(_ptr(X)), ctypes.c_int64(n), ctypes.c_int32(d),
                                      ctypes.c_int32(nlist), ctypes.c_uint64(seed & (2**64 - 1)),
@@ -221,15 +246,20 @@ class Index:
     def search(self, Q, k: int, nprobe: int, n_rerank: int, *, scan_path: int = SCAN_AUTO,
                rank_key: int = RANK_EST, eps0: float = 0.0, query_id_base: int = 0, cap: int = 0,
                seed_max: int = 0, stream=None, debug: Optional[dict] = None, out=None,
-               profile: Optional[Profile] = None, rerank: int = RERANK_FIXED, query_bits: int = 4):
+               profile: Optional[Profile] = None, rerank: int = RERANK_FIXED, query_bits: int = 4,
+               variant: int = 0):
         """Returns (ids int64 [nq, k], dists float32 [nq, k]) on Q's device.
-        ``debug`` maps rabitq_debug member names to preallocated tensors."""
+        ``debug`` maps rabitq_debug member names to preallocated tensors.
+        Device inputs run on ``stream`` (default: torch's current stream)."""
         torch = _torch()
+        Q0 = Q
         Q = _as_f32(Q)
         nq = Q.shape[0]
+        temps = [Q if Q is not Q0 else None]
         if out is None:
             ids = torch.empty((nq, k), dtype=torch.int64, device=Q.device)
             dists = torch.empty((nq, k), dtype=torch.float32, device=Q.device)
+            temps += [ids, dists]
         else:
             ids, dists = out
         o = SearchOpts()
@@ -238,7 +268,8 @@ class Index:
         o.query_id_base, o.cap_per_query, o.seed_max = query_id_base, cap, seed_max
         o.rerank = rerank
         o.query_bits = query_bits
-        o.stream = _stream_handle(stream)
+        o.variant = variant
+        o.stream = _call_stream(stream, Q, temps)
         dbg = None
         if debug:
             dbg = Debug()
@@ -317,14 +348,17 @@ class Comm:
 
     def search_sharded(self, shard: Index, Q, k, nprobe, n_rerank, **kw):
         torch = _torch()
+        Q0 = Q
         Q = _as_f32(Q)
         nq = Q.shape[0]
         ids = torch.empty((nq, k), dtype=torch.int64, device=Q.device)
         dists = torch.empty((nq, k), dtype=torch.float32, device=Q.device)
         o = SearchOpts()
         lib().rabitq_search_opts_default(ctypes.byref(o))
+        stream = kw.pop("stream", None)
         for key, v in kw.items():
             setattr(o, key, v)
+        o.stream = _call_stream(stream, Q, [Q if Q is not Q0 else None, ids, dists])
         _check(lib().rabitq_search_sharded(shard._h, self._h, ctypes.c_void_p(_ptr(Q)), ctypes.c_int64(nq),
                                            ctypes.c_int32(k), ctypes.c_int32(nprobe), ctypes.c_int32(n_rerank),
                                            ctypes.byref(o), ctypes.c_void_p(_ptr(ids)),

@@ -499,10 +499,12 @@ void build_index(rabitq_index* idx, const float* X, int64_t n, int D, int nlist,
     idx->h_list_off.assign(nlist + 1, 0);
     idx->h_slot_off.assign(nlist + 1, 0);
     idx->max_list = 0;
+    idx->tiles8_sum = 0;
     for (int j = 0; j < nlist; ++j) {
         idx->h_list_off[j + 1] = idx->h_list_off[j] + sizes[j];
         idx->h_slot_off[j + 1] = idx->h_slot_off[j] + ((sizes[j] + 31) / 32) * 32;
         idx->max_list = std::max(idx->max_list, sizes[j]);
+        idx->tiles8_sum += ((sizes[j] + 127) / 128 + 7) / 8;
     }
     idx->nslots = idx->h_slot_off[nlist];
     // one spare 128-slot tile so bulk tile loads past the last list stay in bounds
@@ -557,7 +559,7 @@ void build_index(rabitq_index* idx, const float* X, int64_t n, int D, int nlist,
 
     // ---- expanded codes: the grouped scan's A operand by TMA (when they fit comfortably) ----
     {
-        const char* env = getenv("RABITQ_CODES8");  // "0": not built (the scan expands codes in the kernel)
+        const char* env = rq_diag_env("RABITQ_CODES8");  // "0": not built (the scan expands codes in the kernel)
         size_t freeb = 0, totalb = 0;
         RQ_CUDA(cudaMemGetInfo(&freeb, &totalb));
         const size_t bytes = (size_t)(idx->nslots + 128) * 32 * W;
@@ -569,7 +571,7 @@ void build_index(rabitq_index* idx, const float* X, int64_t n, int D, int nlist,
 
     // ---- slot-ordered vectors for the dense re-rank (when they fit comfortably) ----
     {
-        const char* env = getenv("RABITQ_SLOT_VECTORS");  // "0": never build the copy
+        const char* env = rq_diag_env("RABITQ_SLOT_VECTORS");  // "0": never build the copy
         size_t freeb = 0, totalb = 0;
         RQ_CUDA(cudaMemGetInfo(&freeb, &totalb));
         const size_t bytes = (size_t)(idx->nslots + 128) * D * sizeof(float);

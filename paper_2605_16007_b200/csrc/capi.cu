@@ -257,6 +257,7 @@ static void search_local(const rabitq_index* idx, const float* Q, int64_t nq, in
     RQ_REQUIRE(!cfg.full || (o.scan_path != RABITQ_SCAN_POPC && idx->W <= 32), RABITQ_ERR_UNSUPPORTED,
                "query_bits 32 runs on the grouped tensor-core scan only (d <= 1024)");
     cfg.eps0 = o.eps0 > 0.0f ? o.eps0 : 1.9f;
+    cfg.variant = o.variant;
     // the survivor buffer is cheap HBM (8 B/entry): size it so that overflow
     // re-scans are rare even when the seeded threshold is loose
     cfg.cap = o.cap_per_query > 0 ? o.cap_per_query : std::max(8192, 16 * M);
@@ -266,7 +267,7 @@ static void search_local(const rabitq_index* idx, const float* Q, int64_t nq, in
     cfg.seed_max = o.seed_max > 0 ? std::max(o.seed_max, M) : 0;
     RQ_REQUIRE(cfg.seed_max <= 49152, RABITQ_ERR_INVALID_ARGUMENT, "seed_max too large");
     {
-        const char* rr = getenv("RABITQ_REFINE_RANK");  // diagnostics: tensor-core threshold refinement pass
+        const char* rr = rabitq::rq_diag_env("RABITQ_REFINE_RANK");  // diagnostics: tensor-core threshold refinement pass
         cfg.refine_rank = rr ? atoi(rr) : 0;
     }
 

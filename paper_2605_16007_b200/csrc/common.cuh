@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -91,6 +92,17 @@ __device__ __forceinline__ U4 philox4x32_10(const PhiloxSched& s, U4 c) {
         c = U4{hi1 ^ c.y ^ s.k0[r], lo1, hi0 ^ c.w ^ s.k1[r], lo0};
     }
     return c;
+}
+
+// Diagnostic environment switches exist only in a -DRABITQ_DIAG build: the
+// product library's paths and results never depend on the environment.
+inline const char* rq_diag_env(const char* name) {
+#ifdef RABITQ_DIAG
+    return getenv(name);
+#else
+    (void)name;
+    return nullptr;
+#endif
 }
 
 // --------------------------------------------------- order-preserving keys --

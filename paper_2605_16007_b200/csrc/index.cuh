@@ -18,6 +18,7 @@ struct rabitq_index {
     cudaStream_t side = nullptr;   // search: the re-rank ordering + dense block overlap the scan on it
     int D = 0, W = 0, nlist = 0;
     int64_t n = 0, id_offset = 0, nslots = 0, max_list = 0;
+    int64_t tiles8_sum = 0;        // sum over lists of ceil(ceil(size / 128) / 8) (grouped-scan item bound)
     uint64_t seed = 0;
 
     float* P = nullptr;            // [D x D] row-major, x' = P^T x

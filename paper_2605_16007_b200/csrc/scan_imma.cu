@@ -132,7 +132,7 @@ __device__ __forceinline__ Item decode_item(const ScanArgs& a, int NG, int64_t i
     it.j = (int)lo;
     it.L = __ldg(a.list_off + lo + 1) - __ldg(a.list_off + lo);
     const int64_t gs = __ldg(a.gstart + lo);
-    const int64_t G = __ldg(a.gstart + lo + 1) - gs;
+    const int64_t G = __ldg(a.gcount + lo);
     const int64_t ntl = (it.L + kTM - 1) / kTM;
     const int64_t nti = (ntl + kTilesPerItem - 1) / kTilesPerItem;
     const int64_t local = item - __ldg(a.list_items + lo);
@@ -179,14 +179,6 @@ __device__ __forceinline__ float est_of(uint32_t acc, const ColC& cc, float2 fac
     return __fmaf_rn(-fac.y, tt, __fadd_rn(fac.x, cc.nq2));
 }
 
-// Column constants in shared memory, two columns per 64-byte record so that
-// the fast test of columns 2p, 2p+1 takes (-a, b) and (-K, U) of both with two
-// 16-byte loads, already paired for the packed FP32 ops (FFMA2 / FADD2)
-struct ColPair {
-    float na[2], b[2], nK[2], U[2];
-    float nq2[2], tau[2];
-    int q[2], pair[2];
-};
 __device__ __forceinline__ void colp_put(ColPair* cp, int c, const ColC& x) {
     ColPair& P = cp[c >> 1];
     const int h = c & 1;
@@ -281,7 +273,7 @@ __global__ __launch_bounds__(n_threads(kTA), 1) void scan_imma_kernel(const __gr
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
     uint8_t* smem = smem_raw + pad;
-    const SmemPlan sp = smem_plan(a.Dp, kTA, a.ngmax, a.minst);
+    const SmemPlan sp = smem_plan(a.Dp, kTA);
     uint8_t* Bres = smem;                                        // [nchunks][NG rows][128 B], 128-byte swizzle
     ColPair* colc = reinterpret_cast<ColPair*>(smem + sp.off_colc);  // [2][NG / 2]
     __shared__ __align__(8) uint64_t full_bar[kMaxSlots], empty_bar[kMaxSlots], accf_bar[2], acce_bar[2],
@@ -408,10 +400,6 @@ __global__ __launch_bounds__(n_threads(kTA), 1) void scan_imma_kernel(const __gr
                             // A stage s (TMA, 128-byte swizzle) free once these retire
                             const uint64_t ad = tc::smem_desc_sw128(tc::smem_u32(smem + sp.off_raw + s * kAStage));
                             tc::mma_i8_ss_chunk(dacc, ad, bd, idesc, c > 0 ? 1u : 0u, nks, &empty_bar[s]);
-                        } else if (a.experiment & 2) {  // diagnostics: skip the UMMAs
-                            const uint32_t aaddr = tmemA + (uint32_t)(s * kChunkCols);
-                            if (c == 0) tc::mma_i8_ts_warp(dacc, aaddr, bd, idesc, 0u);
-                            tc::commit_warp(&empty_bar[s]);
                         } else {
                             // nks UMMAs + commit: A slot s free once these retire
                             const uint32_t aaddr = tmemA + (uint32_t)(s * kChunkCols);
@@ -474,7 +462,7 @@ __global__ __launch_bounds__(n_threads(kTA), 1) void scan_imma_kernel(const __gr
         ColC nextc;
         auto fetch_colc = [&](const Item& x) {  // one coalesced 32-byte load per column (NG <= 32 kEpiWarps)
             if (et < x.ncols) {
-                nextc = a.gcolc[x.grow0 + et];
+                nextc = colp_get(a.gcolp, (int)(x.grow0 + et));
             } else {
                 nextc.a = nextc.b = nextc.K = nextc.nq2 = 0.f;
                 nextc.tau = -INFINITY;
@@ -518,7 +506,7 @@ __global__ __launch_bounds__(n_threads(kTA), 1) void scan_imma_kernel(const __gr
                 constexpr int kMaxHC = (kTN / kEC + kEpiWarps / 4 - 1) / (kEpiWarps / 4);
                 uint32_t hc_cols[kMaxHC], hc_bal[kMaxHC];
                 int hc_base[kMaxHC];
-                const int ncols_e = (a.experiment & 1) ? 0 : it.ncols;
+                const int ncols_e = it.ncols;
 #pragma unroll
                 for (int k = 0; k < kMaxHC; ++k) hc_cols[k] = 0u;
 #pragma unroll
@@ -663,231 +651,6 @@ __global__ __launch_bounds__(n_threads(kTA), 1) void scan_imma_kernel(const __gr
     if (warp == kMmaWarp) tc::tmem_dealloc(tmem, kTmemCols);
 }
 
-// ------------------------------------------------- operand-swapped main scan
-// The main scan (rank key EST, no dump / re-scan / dense mode, 4-bit query)
-// with the roles of the operands swapped: the group's <= 128 quantized queries
-// are the A operand, resident in TMEM for a whole item (K = Dp bytes = Dp / 4
-// columns), and each 128-vector code tile is the B operand, streamed from the
-// expanded codes by TMA through kSwB shared-memory stages.  D[query][vector]
-// sits in TMEM with one query per lane, so the epilogue keeps the query's
-// column constants in registers and reserves a lane's survivors of a 16-vector
-// chunk with one counter atomic.  Same arithmetic per (query, vector) as
-// scan_imma_kernel: identical keys and survivors.
-constexpr int kSwNG = 128;        // queries per group (UMMA M)
-constexpr int kSwB = 12;          // code stages (16 KB each)
-constexpr int kSwEpi0 = 6;        // warps 0 loader, 1 MMA, 2-5 query writers, 6-21 epilogue
-constexpr int kSwNT = (kSwEpi0 + kEpiWarps) * 32;
-constexpr int kSwAcc = 128;       // accumulator columns per buffer (128 vectors)
-__global__ __launch_bounds__(kSwNT, 1) void scan_swap_kernel(const __grid_constant__ CUtensorMap tmapC, ScanArgs a) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
-    uint8_t* stages = smem_raw + pad;  // [kSwB][128 vectors][128 bytes], 128-byte swizzle
-    __shared__ __align__(8) uint64_t full_bar[kSwB], empty_bar[kSwB], accf_bar[2], acce_bar[2],
-        afull_bar[kMaxChunks], afree_bar[kMaxChunks], vfull_bar[2];
-    __shared__ __align__(16) float4 vconst[2][kTM / 2];  // per tile buffer: (f0, A0, f1, A1) per vector pair
-    __shared__ __align__(16) float2 vpc[2][kTM / 2];     // (pcf0, pcf1)
-    __shared__ uint32_t vrow[2][kTM];
-    __shared__ uint32_t tmem_base_s;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int nchunks = (a.Dp + kKC - 1) / kKC;
-    if (warp == 1) tc::tmem_alloc(&tmem_base_s, kTmemCols);
-    if (tid == 0) {
-        for (int s = 0; s < kSwB; ++s) {
-            tc::mbar_init(&full_bar[s], 1);
-            tc::mbar_init(&empty_bar[s], 1);
-        }
-        for (int b = 0; b < 2; ++b) {
-            tc::mbar_init(&accf_bar[b], 1);
-            tc::mbar_init(&acce_bar[b], kEpiWarps);
-        }
-        for (int c = 0; c < kMaxChunks; ++c) {
-            tc::mbar_init(&afull_bar[c], 4);  // one arrive per query-writer warp
-            tc::mbar_init(&afree_bar[c], 1);
-        }
-        tc::prefetch_tmap(&tmapC);
-    }
-    tc::fence_before_sync();
-    __syncthreads();
-    tc::fence_after_sync();
-    const uint32_t tmem = tmem_base_s;
-    const uint32_t tmemA = tmem + 2u * kSwAcc;  // the queries: Dp / 4 columns
-    const int64_t total = a.list_items[a.nlist];
-
-    if (warp == 0) {
-        // ================= code tiles (B) by TMA =================
-        if (lane == 0) {
-            uint32_t gc = 0;
-            for (int64_t item = blockIdx.x; item < total; item += gridDim.x) {
-                const Item it = decode_item(a, kSwNG, item);
-                for (int t = 0; t < it.ntiles; ++t) {
-                    const int row0 = (int)(it.slot_base + (it.t0 + t) * kTM);
-                    for (int c = 0; c < nchunks; ++c, ++gc) {
-                        const int s = (int)(gc % kSwB);
-                        const uint32_t u = gc / kSwB;
-                        if (u > 0) tc::mbar_wait_backoff(&empty_bar[s], (u - 1) & 1);
-                        tc::mbar_arrive_expect_tx(&full_bar[s], (uint32_t)kAStage);
-                        tc::tma_load_2d(stages + s * kAStage, &tmapC, &full_bar[s], c * kKC, row0);
-                    }
-                }
-            }
-        }
-    } else if (warp == 1) {
-        // ================= MMA issuer =================
-        uint32_t gc = 0, tcnt = 0, ic = 0;
-        const uint32_t idesc = tc::idesc_i8(kSwNG, kTM, /*a_signed=*/false, /*b_signed=*/true);
-        for (int64_t item = blockIdx.x; item < total; item += gridDim.x, ++ic) {
-            const Item it = decode_item(a, kSwNG, item);
-            for (int t = 0; t < it.ntiles; ++t, ++tcnt) {
-                const int b = tcnt & 1;
-                const uint32_t ub = tcnt >> 1;
-                if (ub > 0) tc::mbar_wait_backoff(&acce_bar[b], (ub - 1) & 1);
-                tc::fence_after_sync();
-                const uint32_t dacc = tmem + (uint32_t)b * kSwAcc;
-                for (int c = 0; c < nchunks; ++c, ++gc) {
-                    const int s = (int)(gc % kSwB);
-                    const int nks = min(kKC, a.Dp - c * kKC) / 32;
-                    if (t == 0) tc::mbar_wait(&afull_bar[c], ic & 1);  // the item's query chunk c is in TMEM
-                    tc::mbar_wait(&full_bar[s], (gc / kSwB) & 1);
-                    tc::fence_after_sync();
-                    const uint64_t bd = tc::smem_desc_sw128(tc::smem_u32(stages + s * kAStage));
-                    tc::mma_i8_ts_chunk(dacc, tmemA + (uint32_t)(c * kChunkCols), bd, idesc, c > 0 ? 1u : 0u, nks,
-                                        &empty_bar[s]);
-                    if (t == it.ntiles - 1) tc::commit_warp(&afree_bar[c]);  // query chunk c free for the next item
-                    if (c == nchunks - 1) tc::commit_warp(&accf_bar[b]);
-                }
-            }
-        }
-    } else if (warp < kSwEpi0) {
-        // ================= queries (A) into TMEM =================
-        const int qq = warp & 3;              // TMEM lane quarter of this warp
-        const int r = qq * 32 + lane;         // query row of the group = TMEM lane
-        const uint32_t lane_addr = (uint32_t)(qq * 32) << 16;
-        uint32_t ic = 0;
-        for (int64_t item = blockIdx.x; item < total; item += gridDim.x, ++ic) {
-            const Item it = decode_item(a, kSwNG, item);
-            const uint4* src = reinterpret_cast<const uint4*>(a.qbar8 + (size_t)(it.grow0 + r) * a.Dp);
-            const bool ok = r < it.ncols;
-            for (int c = 0; c < nchunks; ++c) {
-                // chunk c (128 K bytes = 32 columns) once the previous item's last tile used it
-                uint4 v[8];
-                const int nq4 = min(kKC, a.Dp - c * kKC) / 16;  // 16-byte words in this chunk (4 or 8)
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    v[k] = (ok && k < nq4) ? __ldg(src + c * 8 + k) : make_uint4(0u, 0u, 0u, 0u);
-                if (ic > 0) tc::mbar_wait_backoff(&afree_bar[c], (ic - 1) & 1);
-                tc::fence_after_sync();
-                const uint32_t dst = tmemA + lane_addr + (uint32_t)(c * kChunkCols);
-                tc::tmem_st16(dst, v[0], v[1], v[2], v[3]);
-                if (nq4 > 4) tc::tmem_st16(dst + 16, v[4], v[5], v[6], v[7]);
-                tc::tmem_st_wait();
-                tc::fence_before_sync();
-                __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&afull_bar[c]);
-            }
-        }
-    } else {
-        // ================= epilogue: lane = query, columns = vectors =================
-        const int e = warp - kSwEpi0;
-        const int quarter = warp & 3;
-        const int part = e >> 2;              // column chunks part, part + 4 (16 vectors each)
-        const int r = quarter * 32 + lane;    // query row of the group
-        uint32_t tcnt = 0;
-        for (int64_t item = blockIdx.x; item < total; item += gridDim.x) {
-            const Item it = decode_item(a, kSwNG, item);
-            const bool qok = r < it.ncols;
-            ColC cc;
-            if (qok) {
-                cc = a.gcolc[it.grow0 + r];
-            } else {
-                cc.a = cc.b = cc.K = cc.nq2 = 0.f;
-                cc.tau = cc.U = -INFINITY;
-                cc.q = 0;
-                cc.pair = -1;
-            }
-            const float2 nb_pc = make_float2(cc.b, cc.b), nK2 = make_float2(-cc.K, -cc.K);
-            const float2 na2 = make_float2(-cc.a, -cc.a), mg2 = make_float2(12582912.0f, 12582912.0f);
-            for (int t = 0; t < it.ntiles; ++t, ++tcnt) {
-                const int b = tcnt & 1;
-                const uint32_t ub = tcnt >> 1;
-                const int64_t vbase = (it.t0 + t) * kTM;
-                {
-                    // the tile's vector constants in shared memory (double-buffered by tile
-                    // parity; the barrier below also ends every warp's use of this buffer
-                    // two tiles ago): (-f0, -f1, A0, A1), (pcf0, pcf1), rows
-                    const int et = e * 32 + lane;
-                    if (et < kTM / 2) {
-                        const int64_t v0 = vbase + 2 * et;
-                        const bool ok0 = v0 < it.L, ok1 = v0 + 1 < it.L;
-                        const float2 f0 = ok0 ? __ldg(a.fac + it.slot_base + v0) : make_float2(0.f, 0.f);
-                        const float2 f1 = ok1 ? __ldg(a.fac + it.slot_base + v0 + 1) : make_float2(0.f, 0.f);
-                        vconst[b][et] = make_float4(-f0.y, -f1.y, f0.x, f1.x);
-                        vpc[b][et] = make_float2(ok0 ? (float)__ldg(a.pcnt + it.slot_base + v0) : 0.f,
-                                                 ok1 ? (float)__ldg(a.pcnt + it.slot_base + v0 + 1) : 0.f);
-                    } else if (et < kTM / 2 + kTM) {
-                        const int64_t v = vbase + (et - kTM / 2);
-                        vrow[b][et - kTM / 2] = v < it.L ? __ldg(a.rows + it.slot_base + v) : 0u;
-                    }
-                    tc::named_barrier(1, kEpiWarps * 32);
-                }
-                tc::mbar_wait(&accf_bar[b], ub & 1);
-                tc::fence_after_sync();
-                uint32_t hc_bits[2];
-                int hc_base[2];
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    const int col0 = (part + 4 * k) * 16;
-                    const uint32_t tcol = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)b * kSwAcc + col0;
-                    uint32_t acc[16];
-                    tc::tmem_ld16(tcol, acc);
-                    uint32_t bits = 0u;
-                    const int64_t nval = it.L - (vbase + col0);  // valid vectors from col0 on
-#pragma unroll
-                    for (int i = 0; i < 16; i += 2) {
-                        const float4 vc = vconst[b][(col0 + i) >> 1];
-                        const float2 pc = vpc[b][(col0 + i) >> 1];
-                        const float2 ipn = fsub2(make_float2(__int_as_float(0x4B400000 + (int)acc[i]),
-                                                             __int_as_float(0x4B400000 + (int)acc[i + 1])), mg2);
-                        const float2 inner = ffma2(nb_pc, pc, nK2);
-                        const float2 tt = ffma2(na2, ipn, inner);
-                        const float2 vv = ffma2(make_float2(vc.x, vc.y), tt, make_float2(vc.z, vc.w));
-                        bits |= (vv.x <= cc.U ? 1u : 0u) << i;
-                        bits |= (vv.y <= cc.U ? 1u : 0u) << (i + 1);
-                    }
-                    if (nval < 16) bits &= nval > 0 ? (1u << nval) - 1u : 0u;
-                    if (!qok) bits = 0u;
-                    hc_bits[k] = bits;
-                    hc_base[k] = bits ? atomicAdd(&a.cnt[cc.q], __popc(bits)) : 0;
-                }
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    const uint32_t bits = hc_bits[k];
-                    uint32_t cols = __reduce_or_sync(0xFFFFFFFFu, bits);
-                    const int col0 = (part + 4 * k) * 16;
-                    const uint32_t tcol = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)b * kSwAcc + col0;
-                    for (; cols; cols &= cols - 1) {
-                        const int i = __ffs(cols) - 1;
-                        const uint32_t acci = tc::tmem_ld1(tcol + (uint32_t)i);
-                        if ((bits >> i) & 1u) {
-                            const int c = col0 + i;
-                            const float4 vc = vconst[b][c >> 1];
-                            const float2 pc = vpc[b][c >> 1];
-                            const float2 fac = (c & 1) ? make_float2(vc.w, -vc.y) : make_float2(vc.z, -vc.x);
-                            const float key = est_of(acci, cc, fac, (c & 1) ? pc.y : pc.x);
-                            const int pos = hc_base[k] + __popc(bits & ((1u << i) - 1u));
-                            if (pos < a.cap) a.buf[(size_t)cc.q * a.cap + pos] = make_key(key, vrow[b][c]);
-                        }
-                    }
-                }
-                tc::fence_before_sync();
-                __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&acce_bar[b]);
-            }
-        }
-    }
-    tc::fence_before_sync();
-    __syncthreads();
-    if (warp == 1) tc::tmem_dealloc(tmem, kTmemCols);
-}
 
 // ------------------------------------------------------------ list grouping
 // pairs to group: all (sub == nullptr) or the listed pair indices
@@ -934,15 +697,18 @@ __global__ void compact_flagged_kernel(const int* __restrict__ flags, int max_ra
     }
 }
 
-// column constants of every grouped row (one 32-byte record per (query, list) pair)
+// column constants of every grouped row (one half of a 64-byte ColPair record
+// per (query, list) pair; pad rows (gpair < 0) are left untouched: every
+// consumer masks columns past the group's size)
 // (re-scan: tau / pair carry the 64-bit (key, row) threshold instead)
-__global__ void colc_kernel(const int32_t* __restrict__ gpair, int64_t npairs, int nprobe, int D,
+__global__ void colc_kernel(const int32_t* __restrict__ gpair, int64_t nrows, int nprobe, int D,
                             const float4* __restrict__ qscal, const float* __restrict__ tau,
                             const uint64_t* __restrict__ tau64, float eps0, const int64_t* __restrict__ dbase,
                             const int64_t* __restrict__ doff, const int32_t* __restrict__ probes,
-                            const float* __restrict__ list_amax, ColC* __restrict__ gcolc) {
-    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < npairs; g += (int64_t)gridDim.x * blockDim.x) {
+                            const float* __restrict__ list_amax, ColPair* __restrict__ gcolp) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < nrows; g += (int64_t)gridDim.x * blockDim.x) {
         const int p = gpair[g];
+        if (p < 0) continue;
         const int q = p / nprobe;
         const PairC pc = pair_consts(qscal[p], D);
         ColC cc;
@@ -972,8 +738,13 @@ __global__ void colc_kernel(const int32_t* __restrict__ gpair, int64_t npairs, i
             const float mag = __fadd_rn(__fadd_rn(amax, pc.nq2), fabsf(cc.tau));
             cc.U = __fadd_rn(__fsub_rn(cc.tau, pc.nq2), __fmul_rn(4.76837158e-7f, mag));  // 2^-21
         }
-        gcolc[g] = cc;
+        colp_put(gcolp, (int)g, cc);
     }
+}
+
+__global__ void pad_rows_kernel(int nlist, const int64_t* __restrict__ gcount, int64_t* __restrict__ gsz) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= nlist; j += gridDim.x * blockDim.x)
+        gsz[j] = j == nlist ? 0 : (gcount[j] + kBoxRows - 1) / kBoxRows * kBoxRows;
 }
 
 __global__ void list_items_kernel(int nlist, const int64_t* __restrict__ list_off, const int64_t* __restrict__ gcount,
@@ -1005,41 +776,380 @@ __global__ void expand_codes_kernel(const uint32_t* __restrict__ codes, int64_t 
     }
 }
 
-__global__ void list_items_gstart_kernel(int nlist, const int64_t* __restrict__ list_off,
-                                         const int64_t* __restrict__ gstart, int NG, int64_t* __restrict__ items) {
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= nlist; j += gridDim.x * blockDim.x) {
-        if (j == nlist) {
-            items[j] = 0;
-            continue;
-        }
+// ----------------------------------------------------- small-K grouped scan
+// Dp <= 128 (CFG1, CFG3, CFG4, CFG5): one tile pass is a single K chunk, at
+// most 4 UMMAs of M = 128, so the epilogue -- one TMEM read, the estimator
+// and the threshold test per (query, vector) pair -- sets the pace.
+// scan_imma_kernel above keeps all 16 epilogue warps on one tile with two
+// accumulators and an item-wide barrier, which serialised every tile's
+// latency chain (CFG4: 13.5 ms, issue active 47 %; ncu: 10 % of the stall
+// samples on the per-tile row loads, 7 % on the tail, 8 % of the
+// instructions in decode_item's binary search).  Here:
+//  * the unit of epilogue work is (tile, block of <= 64 group columns): one
+//    of 8 TMEM accumulator slots of 64 columns; units are dealt round-robin
+//    to 4 epilogue warpgroups (4 warps = the 4 TMEM lane quarters), so up to
+//    8 units are in flight and a wide group keeps every warpgroup busy;
+//  * the unit's per-vector constants (n_o^2 and f, popcount, row id, g1) are
+//    staged in shared memory by bulk copies next to the accumulator slot;
+//  * items (list, group of <= 256 queries, <= 8 tiles) come from a table
+//    built once per launch and are taken dynamically (one atomic per item, no
+//    tail) through a shared-memory ring of item records and their column
+//    constants; the query operand (B) is double-buffered per item;
+//  * every wait suspends in hardware (mbarrier.try_wait), no polling loops.
+// Same per-pair arithmetic as scan_imma_kernel (est_of, the fast test), so the
+// keys and survivors are bit-identical (tested).
+constexpr int kSkNG = 256;                                   // group columns (B rows)
+constexpr int kSkUW = 64;                                    // unit width (accumulator slot columns)
+constexpr int kSkRI = 6;                                     // item ring
+constexpr int kSkSA = 5;                                     // A stages (16 KB)
+constexpr int kSkUS = kTmemCols / kSkUW;                     // 8 units in flight
+constexpr int kSkEpi0 = 3;                                   // warps 0 sched + B, 1 A + row constants, 2 MMA
+constexpr int kSkNT = (kSkEpi0 + kEpiWarps) * 32;            // 608 threads
+constexpr uint32_t kSkBStage = kSkNG * kKC;                  // 32 KB
+constexpr uint32_t kSkCStage = kSkNG / 2 * sizeof(ColPair);  // 8 KB
+struct SkRows {                                              // one unit's per-vector constants
+    float2 fac[kTM];
+    float g1[kTM];
+    uint32_t rows[kTM];
+    uint16_t pcnt[kTM];
+};
+constexpr uint32_t kSkOffA = 2 * kSkBStage;
+constexpr uint32_t kSkOffC = kSkOffA + kSkSA * kAStage;
+constexpr uint32_t kSkOffR = kSkOffC + kSkRI * kSkCStage;
+constexpr uint32_t kSkSmem = kSkOffR + kSkUS * sizeof(SkRows) + 1024;  // + alignment slack
+
+// item record: x = first slot of the list, y = its vectors (or sample prefix),
+// z = first grouped row of the group, w = ncols | ntiles << 9 | t0 << 13 (t0 =
+// first tile of the item in the list); w = 0 ends the work.  One warp per list.
+__global__ void item_table_kernel(int nlist, const int64_t* __restrict__ list_off,
+                                  const int64_t* __restrict__ slot_off, const int64_t* __restrict__ gstart,
+                                  const int64_t* __restrict__ gcount, const int64_t* __restrict__ list_items,
+                                  int4* __restrict__ items) {
+    const int lane = threadIdx.x & 31;
+    for (int j = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); j < nlist;
+         j += (int)(((int64_t)gridDim.x * blockDim.x) >> 5)) {
+        const int64_t i0 = list_items[j], ni = list_items[j + 1] - i0;
+        if (ni == 0) continue;
         const int64_t L = list_off[j + 1] - list_off[j];
-        const int64_t G = gstart[j + 1] - gstart[j];
+        const int64_t G = gcount[j];
         const int64_t ntl = (L + kTM - 1) / kTM;
-        items[j] = ((ntl + kTilesPerItem - 1) / kTilesPerItem) * ((G + NG - 1) / NG);
+        const int64_t nti = (ntl + kTilesPerItem - 1) / kTilesPerItem;
+        const int sb = (int)slot_off[j], gs = (int)gstart[j];
+        for (int64_t l = lane; l < ni; l += 32) {
+            const int64_t g = l / nti, ti = l % nti;
+            const int t0 = (int)(ti * kTilesPerItem);
+            const int nt = (int)(ntl - t0 < kTilesPerItem ? ntl - t0 : kTilesPerItem);
+            const int nc = (int)(G - g * kSkNG < kSkNG ? G - g * kSkNG : kSkNG);
+            items[i0 + l] = make_int4(sb, (int)L, gs + (int)(g * kSkNG), nc | nt << 9 | t0 << 13);
+        }
     }
 }
 
+// kMode: 0 main scan (fast test, survivors), 1 re-scan (exact (key, row) <=
+// tau64), 2 dense key dump (threshold sample); kDump (main scan): also write
+// every pair's ip and estimate to the debug dump (exact test path)
+template <bool kLB, int kMode, bool kDump>
+__global__ __launch_bounds__(kSkNT, 1) void scan_small_kernel(const __grid_constant__ CUtensorMap tmapB,
+                                                              const __grid_constant__ CUtensorMap tmapA,
+                                                              ScanArgs a, const int4* __restrict__ items,
+                                                              int* __restrict__ sched) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
+    uint8_t* smem = smem_raw + pad;  // [2] B | [kSkSA] A | [kSkRI] column constants | [kSkUS] unit rows
+    ColPair* colc = reinterpret_cast<ColPair*>(smem + kSkOffC);
+    SkRows* urows = reinterpret_cast<SkRows*>(smem + kSkOffR);
+    __shared__ int4 rec[kSkRI];
+    __shared__ __align__(8) uint64_t ifull[kSkRI], iempty[kSkRI], bfull[2], bfree[2], afull[kSkSA], aempty[kSkSA],
+        accf[kSkUS], acce[kSkUS], rowf[kSkUS];
+    __shared__ uint32_t tmem_base_s;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (warp == 2) tc::tmem_alloc(&tmem_base_s, kTmemCols);
+    if (tid == 0) {
+        for (int s = 0; s < kSkRI; ++s) {
+            tc::mbar_init(&ifull[s], 1);
+            tc::mbar_init(&iempty[s], 2 + kEpiWarps);  // A loader, MMA warp, every epilogue warp
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&bfull[b], 1);
+            tc::mbar_init(&bfree[b], 1);
+        }
+        for (int s = 0; s < kSkSA; ++s) {
+            tc::mbar_init(&afull[s], 1);
+            tc::mbar_init(&aempty[s], 1);
+        }
+        for (int k = 0; k < kSkUS; ++k) {
+            tc::mbar_init(&accf[k], 1);
+            tc::mbar_init(&acce[k], 4);  // the 4 warps of the unit's warpgroup
+            tc::mbar_init(&rowf[k], 1);
+        }
+        tc::prefetch_tmap(&tmapB);
+        tc::prefetch_tmap(&tmapA);
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = tmem_base_s;
+    const int64_t nitems = a.list_items[a.nlist];
+
+    if (warp == 0) {
+        // ============ scheduler: item records, column constants, query operand (B) ============
+        if (lane == 0) {
+            for (uint32_t i = 0;; ++i) {
+                const int s = (int)(i % kSkRI);
+                if (i >= (uint32_t)kSkRI) tc::mbar_wait(&iempty[s], ((i / kSkRI) - 1) & 1);
+                const int64_t id = atomicAdd(sched, 1);
+                if (id >= nitems) {
+                    rec[s] = make_int4(0, 0, 0, 0);
+                    tc::mbar_arrive(&ifull[s]);
+                    break;
+                }
+                const int4 r = __ldg(items + id);
+                rec[s] = r;
+                const int nc = r.w & 511;
+                const uint32_t cb = (uint32_t)(((nc + 15) & ~15) / 2) * (uint32_t)sizeof(ColPair);
+                tc::mbar_arrive_expect_tx(&ifull[s], cb);
+                tc::bulk_load(colc + s * (kSkNG / 2), a.gcolp + r.z / 2, cb, &ifull[s]);
+                const int b = (int)(i & 1u);
+                if (i >= 2) tc::mbar_wait(&bfree[b], ((i >> 1) - 1) & 1);
+                const int nb = (nc + kBoxRows - 1) / kBoxRows;
+                tc::mbar_arrive_expect_tx(&bfull[b], (uint32_t)(nb * kBoxRows * kKC));
+                for (int bx = 0; bx < nb; ++bx)
+                    tc::tma_load_2d(smem + b * kSkBStage + bx * kBoxRows * kKC, &tmapB, &bfull[b], 0,
+                                    r.z + bx * kBoxRows);
+            }
+        }
+    } else if (warp == 1) {
+        // ============ code operand (A) by TMA, per-vector constants by bulk copies ============
+        if (lane == 0) {
+            uint32_t tcnt = 0, ucnt = 0;
+            for (uint32_t i = 0;; ++i) {
+                const int s = (int)(i % kSkRI);
+                tc::mbar_wait(&ifull[s], (i / kSkRI) & 1);
+                const int4 r = rec[s];
+                tc::mbar_arrive(&iempty[s]);
+                if (r.w == 0) break;
+                const int nc = r.w & 511, nt = (r.w >> 9) & 15, t0 = (int)((uint32_t)r.w >> 13);
+                const int nu = (nc + kSkUW - 1) / kSkUW;
+                for (int t = 0; t < nt; ++t, ++tcnt) {
+                    const int st = (int)(tcnt % kSkSA);
+                    if (tcnt >= (uint32_t)kSkSA) tc::mbar_wait(&aempty[st], ((tcnt / kSkSA) - 1) & 1);
+                    tc::mbar_arrive_expect_tx(&afull[st], (uint32_t)kAStage);
+                    const int v0 = (t0 + t) * kTM;
+                    tc::tma_load_2d(smem + kSkOffA + st * kAStage, &tmapA, &afull[st], 0, r.x + v0);
+                    const int nv = r.y - v0 < kTM ? r.y - v0 : kTM;
+                    const uint32_t ncp = (uint32_t)((nv + 31) & ~31);  // whole 32-slot blocks of the list
+                    const int64_t s0 = (int64_t)r.x + v0;
+                    for (int u = 0; u < nu; ++u, ++ucnt) {
+                        const int k = (int)(ucnt % kSkUS);
+                        if (ucnt >= (uint32_t)kSkUS) tc::mbar_wait(&acce[k], ((ucnt / kSkUS) - 1) & 1);
+                        SkRows& R = urows[k];
+                        tc::mbar_arrive_expect_tx(&rowf[k], ncp * ((kLB ? 18u : 14u)));
+                        tc::bulk_load(R.fac, a.fac + s0, ncp * 8u, &rowf[k]);
+                        tc::bulk_load(R.pcnt, a.pcnt + s0, ncp * 2u, &rowf[k]);
+                        tc::bulk_load(R.rows, a.rows + s0, ncp * 4u, &rowf[k]);
+                        if (kLB) tc::bulk_load(R.g1, a.g1 + s0, ncp * 4u, &rowf[k]);
+                    }
+                }
+            }
+        }
+    } else if (warp == 2) {
+        // ============ MMA issuer: per unit nks UMMAs (N <= 64) into slot ucnt % 8 ============
+        uint32_t tcnt = 0, ucnt = 0;
+        const int nks = a.Dp / 32;
+        for (uint32_t i = 0;; ++i) {
+            const int s = (int)(i % kSkRI);
+            tc::mbar_wait(&ifull[s], (i / kSkRI) & 1);
+            const int4 r = rec[s];
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&iempty[s]);
+            if (r.w == 0) break;
+            const int nc = r.w & 511, nt = (r.w >> 9) & 15;
+            const int nu = (nc + kSkUW - 1) / kSkUW;
+            const int b = (int)(i & 1u);
+            tc::mbar_wait(&bfull[b], (i >> 1) & 1);
+            tc::fence_after_sync();
+            const uint32_t bbase = tc::smem_u32(smem + b * kSkBStage);
+            for (int t = 0; t < nt; ++t, ++tcnt) {
+                const int as = (int)(tcnt % kSkSA);
+                tc::mbar_wait(&afull[as], (tcnt / kSkSA) & 1);
+                tc::fence_after_sync();
+                const uint64_t adesc = tc::smem_desc_sw128(tc::smem_u32(smem + kSkOffA + as * kAStage));
+                for (int u = 0; u < nu; ++u, ++ucnt) {
+                    const int k = (int)(ucnt % kSkUS);
+                    if (ucnt >= (uint32_t)kSkUS) {
+                        tc::mbar_wait(&acce[k], ((ucnt / kSkUS) - 1) & 1);
+                        tc::fence_after_sync();
+                    }
+                    const int w = nc - u * kSkUW < kSkUW ? nc - u * kSkUW : kSkUW;
+                    const uint32_t idesc = tc::idesc_i8(kTM, (w + 15) & ~15, /*a_signed=*/true);
+                    // B rows [64 u, 64 u + w): 64 rows = 8 swizzle atoms further
+                    const uint64_t bdesc = tc::smem_desc_sw128(bbase + (uint32_t)(u * kSkUW * kKC));
+                    tc::mma_i8_ss_chunk(tmem + (uint32_t)(k * kSkUW), adesc, bdesc, idesc, 0u, nks, &accf[k]);
+                }
+                tc::commit_warp(&aempty[as]);                // the tile's code operand is free
+                if (t == nt - 1) tc::commit_warp(&bfree[b]);  // the item's query operand is free
+            }
+        }
+    } else {
+        // ============ epilogue: warpgroup (unit % 4), 32 rows x the unit's columns per warp ============
+        const int e = warp - kSkEpi0, wg = e >> 2, quarter = warp & 3;
+        const int r = quarter * 32 + lane;
+        const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+        uint32_t ucnt = 0;
+        for (uint32_t i = 0;; ++i) {
+            const int s = (int)(i % kSkRI);
+            tc::mbar_wait(&ifull[s], (i / kSkRI) & 1);
+            const int4 R = rec[s];
+            if (R.w == 0) break;
+            const int nc = R.w & 511, nt = (R.w >> 9) & 15, t0 = (int)((uint32_t)R.w >> 13);
+            const int nu = (nc + kSkUW - 1) / kSkUW;
+            for (int t = 0; t < nt; ++t) {
+                const int64_t v = (int64_t)(t0 + t) * kTM + r;
+                const bool vok = v < R.y;
+                for (int u = 0; u < nu; ++u, ++ucnt) {
+                    if ((int)(ucnt & 3u) != wg) continue;
+                    const int k = (int)(ucnt % kSkUS);
+                    const uint32_t ph = (ucnt / kSkUS) & 1;
+                    const ColPair* cb = colc + s * (kSkNG / 2) + u * (kSkUW / 2);
+                    const int w = nc - u * kSkUW < kSkUW ? nc - u * kSkUW : kSkUW;
+                    tc::mbar_wait(&rowf[k], ph);
+                    const SkRows& RS = urows[k];
+                    const float2 fac = vok ? RS.fac[r] : make_float2(0.f, 0.f);
+                    const float pcf = vok ? (float)RS.pcnt[r] : 0.f;
+                    const float g1 = (kLB && vok) ? RS.g1[r] : 0.f;
+                    const uint32_t row = vok ? RS.rows[r] : 0u;
+                    tc::mbar_wait(&accf[k], ph);
+                    tc::fence_after_sync();
+                    const uint32_t tbase = lane_base + (uint32_t)(k * kSkUW);
+                    uint32_t hc_cols[4], hc_bal[4];
+                    int hc_base[4];
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        hc_cols[h] = 0u;
+                        hc_bal[h] = 0u;
+                        hc_base[h] = 0;
+                        const int col0 = h * kEC;
+                        if (col0 < w) {
+                            uint32_t acc[kEC];
+                            tc::tmem_ld16(tbase + (uint32_t)col0, acc);
+                            if constexpr (kMode == 2) {
+                                // sample scan: every key, coalesced (lanes = consecutive vectors)
+                                if (vok) {
+#pragma unroll
+                                    for (int i2 = 0; i2 < kEC; ++i2) {
+                                        if (col0 + i2 < w) {
+                                            const ColC cc = colp_get(cb, col0 + i2);
+                                            const float key = rank_key<kLB>(est_of(acc[i2], cc, fac, pcf), epsnq_of(cc), g1);
+                                            const int64_t off = ((int64_t)(uint32_t)cc.pair << 32) | (uint32_t)cc.q;
+                                            a.dense_keys[off + v] = f2o(key);
+                                        }
+                                    }
+                                }
+                            } else {
+                                uint32_t rowbits = 0u;
+                                if constexpr (!kLB && kMode == 0 && !kDump) {
+                                    // fast test, two columns per packed op: v = fma(-f, fma(-a, ipn,
+                                    // fma(b, pcf, -K)), A) <= U <=> U - v >= 0 (sign bit clear; the
+                                    // difference of two floats is never -0 when v > U).  Sign bits
+                                    // are shifted in from the last column down (one SHF per column).
+                                    const float2 pc2 = make_float2(pcf, pcf), nf2 = make_float2(-fac.y, -fac.y);
+                                    const float2 fx2 = make_float2(fac.x, fac.x), mg2 = make_float2(12582912.0f, 12582912.0f);
+                                    const float4* P0 = reinterpret_cast<const float4*>(cb + (col0 >> 1));
+                                    uint32_t neg = 0u;
+#pragma unroll
+                                    for (int i2 = kEC - 2; i2 >= 0; i2 -= 2) {
+                                        const float4* P = P0 + 2 * i2;
+                                        const float4 ab = P[0], ku = P[1];  // (-a0, -a1, b0, b1), (-K0, -K1, U0, U1)
+                                        const float2 ipn = fsub2(make_float2(__int_as_float(0x4B400000 + (int)acc[i2]),
+                                                                             __int_as_float(0x4B400000 + (int)acc[i2 + 1])),
+                                                                 mg2);
+                                        const float2 inner = ffma2(make_float2(ab.z, ab.w), pc2, make_float2(ku.x, ku.y));
+                                        const float2 tt = ffma2(make_float2(ab.x, ab.y), ipn, inner);
+                                        const float2 vv = ffma2(nf2, tt, fx2);
+                                        const float2 dd = fsub2(make_float2(ku.z, ku.w), vv);
+                                        neg = __funnelshift_l(__float_as_uint(dd.y), neg, 1);  // (neg << 1) | sign
+                                        neg = __funnelshift_l(__float_as_uint(dd.x), neg, 1);
+                                    }
+                                    rowbits = ~neg & 0xFFFFu;
+                                } else {
+#pragma unroll
+                                    for (int i2 = 0; i2 < kEC; ++i2) {
+                                        const ColC cc = colp_get(cb, col0 + i2);
+                                        const float est = est_of(acc[i2], cc, fac, pcf);
+                                        const float key = rank_key<kLB>(est, epsnq_of(cc), g1);
+                                        if constexpr (kDump) {
+                                            if (vok && col0 + i2 < w) {
+                                                const int64_t di = (a.item_off[cc.pair] + (v >> 5)) * 32 + (v & 31);
+                                                if (di < a.dump_cap) {
+                                                    a.dump_ip[di] = -(int)acc[i2];
+                                                    a.dump_est[di] = est;
+                                                }
+                                            }
+                                        }
+                                        bool sv;
+                                        if constexpr (kMode == 1) {  // exact (key, row) <= tau64
+                                            const uint32_t ko = f2o(key), to = f2o(cc.tau);
+                                            sv = ko < to || (ko == to && row <= (uint32_t)cc.pair);
+                                        } else {
+                                            sv = key <= cc.tau;
+                                        }
+                                        rowbits |= sv ? (1u << i2) : 0u;
+                                    }
+                                }
+                                const int rem = w - col0;
+                                if (rem < kEC) rowbits &= (1u << rem) - 1u;
+                                if (!vok) rowbits = 0u;
+                                const uint32_t cols = __reduce_or_sync(0xFFFFFFFFu, rowbits);
+                                hc_cols[h] = cols;
+                                if (cols) {
+                                    uint32_t mybal = 0u;
+                                    for (uint32_t m = cols; m; m &= m - 1) {
+                                        const int i2 = __ffs(m) - 1;
+                                        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, (rowbits >> i2) & 1u);
+                                        if (lane == i2) mybal = bal;
+                                    }
+                                    hc_bal[h] = mybal;
+                                    if (mybal) hc_base[h] = atomicAdd(&a.cnt[colp_get(cb, col0 + (lane & (kEC - 1))).q], __popc(mybal));
+                                }
+                            }
+                        }
+                    }
+                    if constexpr (kMode != 2) {
+                        // survivors re-read their accumulator column and store (key, row)
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            const uint32_t cols = hc_cols[h];
+                            if (!cols) continue;
+                            const int col0 = h * kEC;
+                            for (uint32_t m = cols; m; m &= m - 1) {
+                                const int i2 = __ffs(m) - 1;
+                                const uint32_t bal = __shfl_sync(0xFFFFFFFFu, hc_bal[h], i2);
+                                const int base = __shfl_sync(0xFFFFFFFFu, hc_base[h], i2);
+                                const uint32_t acci = tc::tmem_ld1(tbase + (uint32_t)(col0 + i2));
+                                if ((bal >> lane) & 1u) {
+                                    const ColC cc = colp_get(cb, col0 + i2);
+                                    const float key = rank_key<kLB>(est_of(acci, cc, fac, pcf), epsnq_of(cc), g1);
+                                    const int pos = base + __popc(bal & ((1u << lane) - 1u));
+                                    if (pos < a.cap) a.buf[(size_t)cc.q * a.cap + pos] = make_key(key, row);
+                                }
+                            }
+                        }
+                    }
+                    tc::fence_before_sync();
+                    __syncwarp();
+                    if (lane == 0) tc::mbar_arrive(&acce[k]);  // the slot (accumulator + rows) may be reused
+                }
+            }
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&iempty[s]);
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 2) tc::tmem_dealloc(tmem, kTmemCols);
+}
+
 }  // namespace
-
-// largest group (B columns) of the TMA-A scan: fewer columns leave shared memory
-// for more A stages in flight (diagnostics: RABITQ_TA_NGMAX, multiple of 32)
-int ta_ngmax() {
-    const char* env = getenv("RABITQ_TA_NGMAX");
-    const int v = env ? atoi(env) : kTN;
-    return std::max(kBoxRows, std::min(kTN, v / kBoxRows * kBoxRows));
-}
-
-// fewest A stages of the TMA-A scan (the group shrinks to make room; 16-column steps)
-int ta_minstages() {
-    const char* env = getenv("RABITQ_TA_MINSTAGES");
-    const int v = env ? atoi(env) : kMinAStages;
-    return std::max(2, std::min(kMaxSlots, v));
-}
-
-const uint8_t* codes8_of(const rabitq_index* idx) {
-    const char* env = getenv("RABITQ_CODES8");  // "0": expand in the kernel (diagnostics / tests)
-    return (env && env[0] == '0') ? nullptr : idx->codes8;
-}
 
 void expand_codes(rabitq_index* idx, cudaStream_t st) {
     const size_t bytes = (size_t)(idx->nslots + kTM) * 32 * idx->W;
@@ -1061,41 +1171,53 @@ bool imma_wanted(const rabitq_index* idx, int64_t npairs, int scan_path) {
            idx->W >= 16;
 }
 
+// upper bound on the work items of a grouping with `rows` grouped rows, no
+// list holding more than max_group of them (items of list j = ceil(T_j / 8)
+// ceil(G_j / 256) <= ceil(T_j / 8) (1 + G_j / 256), T_j = tiles of the list)
+int64_t item_bound(const rabitq_index* idx, int64_t rows, int64_t max_group) {
+    const int64_t t8max = ((idx->max_list + kTM - 1) / kTM + kTilesPerItem - 1) / kTilesPerItem;
+    const int64_t b1 = idx->tiles8_sum * ((max_group + kSkNG - 1) / kSkNG);
+    const int64_t b2 = idx->tiles8_sum + t8max * ((rows + kSkNG - 1) / kSkNG);
+    return std::max<int64_t>(1, std::min(b1, b2));
+}
+
 void prepare_groups(const rabitq_index* idx, const int32_t* probes, int64_t n, const int32_t* sub, Groups& g,
-                    cudaStream_t st, int& launches, int rows) {
+                    cudaStream_t st, int& launches, int rows, bool ta) {
     const int nlist = idx->nlist;
     g.Dp = ((idx->D + 31) / 32) * 32;
     g.n = n;
     g.rows = rows;
+    g.ta = ta && idx->codes8 != nullptr;
+    // each list's rows start at a multiple of kBoxRows (pad rows: gpair = -1)
+    g.nrows = n * rows + (int64_t)kBoxRows * nlist + kTN;
     g.gcount.alloc((size_t)nlist + 1, st);
     g.gstart.alloc((size_t)nlist + 1, st);
     g.itemc.alloc((size_t)nlist + 1, st);
     g.list_items.alloc((size_t)nlist + 1, st);
     g.gfill.alloc((size_t)nlist, st);
     g.gpos.alloc((size_t)n, st);
-    g.gpair.alloc((size_t)n * rows + kTN, st);
-    g.qbar8.alloc(((size_t)n * rows + kTN) * g.Dp, st);
+    g.gpair.alloc((size_t)g.nrows, st);
+    g.qbar8.alloc((size_t)g.nrows * g.Dp, st);
     RQ_CUDA(cudaMemsetAsync(g.gcount.p, 0, ((size_t)nlist + 1) * sizeof(int64_t), st));
     RQ_CUDA(cudaMemsetAsync(g.gfill.p, 0, (size_t)nlist * sizeof(int32_t), st));
-    RQ_CUDA(cudaMemsetAsync(g.gpair.p + n * rows, 0, kTN * sizeof(int32_t), st));
+    RQ_CUDA(cudaMemsetAsync(g.gpair.p, 0xFF, (size_t)g.nrows * sizeof(int32_t), st));
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 2048));
     group_count_kernel<<<grid, 256, 0, st>>>(probes, sub, n, g.gcount.p, rows);
     RQ_CHECK_LAUNCH();
+    pad_rows_kernel<<<(nlist + 256) / 256, 256, 0, st>>>(nlist, g.gcount.p, g.itemc.p);
+    RQ_CHECK_LAUNCH();
     size_t tb = 0;
-    RQ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, g.gcount.p, g.gstart.p, nlist + 1, st));
-    size_t tb2 = 0;
-    RQ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, g.itemc.p, g.list_items.p, nlist + 1, st));
+    RQ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, g.itemc.p, g.gstart.p, nlist + 1, st));
     WBuf<uint8_t> tmp;
-    tmp.alloc(std::max(tb, tb2), st);
-    RQ_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, g.gcount.p, g.gstart.p, nlist + 1, st));
+    tmp.alloc(tb, st);
+    RQ_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, g.itemc.p, g.gstart.p, nlist + 1, st));
     group_fill_kernel<<<grid, 256, 0, st>>>(probes, sub, n, g.gstart.p, g.gfill.p, g.gpos.p, g.gpair.p, rows);
     RQ_CHECK_LAUNCH();
-    list_items_kernel<<<(nlist + 256) / 256, 256, 0, st>>>(nlist, idx->list_off, g.gcount.p,
-                                                           group_cols(g.Dp, codes8_of(idx) != nullptr, ta_ngmax(), ta_minstages()),
+    list_items_kernel<<<(nlist + 256) / 256, 256, 0, st>>>(nlist, idx->list_off, g.gcount.p, group_cols(g.Dp, g.ta),
                                                            g.itemc.p);
     RQ_CHECK_LAUNCH();
-    RQ_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb2, g.itemc.p, g.list_items.p, nlist + 1, st));
-    launches += 7;
+    RQ_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, g.itemc.p, g.list_items.p, nlist + 1, st));
+    launches += 8;
 }
 
 void group_items(const rabitq_index* idx, const int64_t* list_off, const Groups& g, WBuf<int64_t>& itemc,
@@ -1104,7 +1226,7 @@ void group_items(const rabitq_index* idx, const int64_t* list_off, const Groups&
     itemc.alloc((size_t)nlist + 1, st);
     items.alloc((size_t)nlist + 1, st);
     list_items_kernel<<<(nlist + 256) / 256, 256, 0, st>>>(nlist, list_off, g.gcount.p,
-                                                           group_cols(g.Dp, codes8_of(idx) != nullptr, ta_ngmax(), ta_minstages()), itemc.p);
+                                                           group_cols(g.Dp, g.ta), itemc.p);
     RQ_CHECK_LAUNCH();
     size_t tb = 0;
     RQ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, itemc.p, items.p, nlist + 1, st));
@@ -1128,7 +1250,7 @@ int64_t regroup_flagged(const rabitq_index* idx, const int32_t* probes, int64_t 
     RQ_CUDA(cudaMemcpyAsync(&n, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     RQ_CUDA(cudaStreamSynchronize(st));
     if (n == 0) return 0;
-    prepare_groups(idx, probes, n, list.p, sub, st, launches, full.rows);
+    prepare_groups(idx, probes, n, list.p, sub, st, launches, full.rows, full.ta);
     const int per = full.rows * full.Dp / 16;
     gather_rows_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(((int64_t)n * per + 255) / 256, 4096)), 256,
                          0, st>>>(list.p, n, full.gpos.p, full.qbar8.p, sub.gpos.p, sub.qbar8.p, full.Dp, full.rows);
@@ -1150,20 +1272,20 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_t st, bool dense) {
-    ScanArgs a = a_in;  // a.npairs = grouped rows (all pairs, or the re-scan's sub list)
-    WBuf<ColC> gcolc;
-    gcolc.alloc((size_t)a.npairs + kTN, st);
-    colc_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((a.npairs + 255) / 256, 2048)), 256, 0, st>>>(
-        a.gpair, a.npairs, a.nprobe, a.D, a.qscal, a.tau, retry ? a.tau64 : nullptr, a.eps0,
-        dense ? a.dense_base : nullptr, dense ? a.dense_off : nullptr, a.probes, a.list_amax, gcolc.p);
+    ScanArgs a = a_in;  // a.nrows = grouped rows allocated (all pairs, or the re-scan's sub list)
+    WBuf<ColPair> gcolp;
+    gcolp.alloc((size_t)(a.nrows + 1) / 2 + kTN, st);
+    colc_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((a.nrows + 255) / 256, 2048)), 256, 0, st>>>(
+        a.gpair, a.nrows, a.nprobe, a.D, a.qscal, a.tau, retry ? a.tau64 : nullptr, a.eps0,
+        dense ? a.dense_base : nullptr, dense ? a.dense_off : nullptr, a.probes, a.list_amax, gcolp.p);
     RQ_CHECK_LAUNCH();
-    a.gcolc = gcolc.p;
+    a.gcolp = gcolp.p;
     int dev = 0, sms = 148;
     RQ_CUDA(cudaGetDevice(&dev));
     RQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    // B = grouped int8 query rows [(npairs + kTN) x Dp]; TMA box 128 bytes x 32 rows, 128-byte swizzle
+    // B = grouped int8 query rows [nrows x Dp]; TMA box 128 bytes x 16 rows, 128-byte swizzle
     CUtensorMap tmap;
-    const cuuint64_t gdim[2] = {(cuuint64_t)a.Dp, (cuuint64_t)(a.npairs + kTN)};
+    const cuuint64_t gdim[2] = {(cuuint64_t)a.Dp, (cuuint64_t)a.nrows};
     const cuuint64_t gstride[1] = {(cuuint64_t)a.Dp};
     const cuuint32_t box[2] = {(cuuint32_t)kKC, (cuuint32_t)kBoxRows};
     const cuuint32_t estr[2] = {1, 1};
@@ -1171,7 +1293,6 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
                                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     RQ_REQUIRE(cr == CUDA_SUCCESS, RABITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
-    // A = expanded codes [(nslots + 128) x Dp] when the index has them: TMA box 128 bytes x 128 rows
     const bool ta = a.codes8 != nullptr;
     CUtensorMap tmapA;
     std::memset(&tmapA, 0, sizeof(tmapA));
@@ -1184,36 +1305,41 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         RQ_REQUIRE(cr == CUDA_SUCCESS, RABITQ_ERR_CUDA, "cuTensorMapEncodeTiled (A) failed: " + std::to_string((int)cr));
     }
-    a.ngmax = ta_ngmax();
-    a.minst = ta_minstages();
-    // operand-swapped main scan (queries resident in TMEM, code tiles streamed
-    // through 12 stages): opt-in (RABITQ_SWAP=1), bit-identical but slower as
-    // built (CFG2 scan 4.47 vs 3.66 ms, CFG3 7.37 vs 4.86 ms): groups of 128
-    // queries (TMEM holds the queries and both 128-column accumulators) mean
-    // more tile passes than the 160 / 256-column groups of scan_imma_kernel
-    const char* sw_env = getenv("RABITQ_SWAP");
-    if (ta && !lb && !dump && !retry && !dense && !a.full && sw_env && sw_env[0] == '1' && a.experiment == 0 &&
-        a.Dp <= 1024) {
-        WBuf<int64_t> itemc, items;
-        itemc.alloc((size_t)a.nlist + 1, st);
-        items.alloc((size_t)a.nlist + 1, st);
-        list_items_gstart_kernel<<<(a.nlist + 256) / 256, 256, 0, st>>>(a.nlist, a.list_off, a.gstart, kSwNG,
-                                                                       itemc.p);
+    if (ta && a.small && a.Dp <= kKC && !a.full && (!dump || !(retry || dense))) {
+        // small-K scan (Dp <= 128): item table, dynamic scheduler
+        RQ_REQUIRE(group_cols(a.Dp, true) == kSkNG && a.items_bound > 0, RABITQ_ERR_INTERNAL,
+                   "small-K scan: group width / item bound");
+        WBuf<int4> items;
+        items.alloc((size_t)a.items_bound, st);
+        WBuf<int> sched;
+        sched.alloc(1, st);
+        RQ_CUDA(cudaMemsetAsync(sched.p, 0, sizeof(int), st));
+        item_table_kernel<<<(unsigned)std::max(1, std::min(a.nlist, 8192) / 8), 256, 0, st>>>(
+            a.nlist, a.list_off, a.slot_off, a.gstart, a.gcount, a.list_items, items.p);
         RQ_CHECK_LAUNCH();
-        size_t tb = 0;
-        RQ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, itemc.p, items.p, a.nlist + 1, st));
-        WBuf<uint8_t> tmp;
-        tmp.alloc(tb, st);
-        RQ_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, itemc.p, items.p, a.nlist + 1, st));
-        ScanArgs s = a;
-        s.list_items = items.p;
-        const size_t smem = (size_t)kSwB * kAStage + 1024;
-        RQ_CUDA(cudaFuncSetAttribute(scan_swap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        scan_swap_kernel<<<sms, kSwNT, smem, st>>>(tmapA, s);
+#define RQ_SMALL(LB, MODE, DP)                                                                                 \
+    do {                                                                                                        \
+        RQ_CUDA(cudaFuncSetAttribute(scan_small_kernel<LB, MODE, DP>,                                           \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSkSmem));               \
+        scan_small_kernel<LB, MODE, DP><<<sms, kSkNT, kSkSmem, st>>>(tmap, tmapA, a, items.p, sched.p);         \
+    } while (0)
+        const int mode = dense ? 2 : retry ? 1 : 0;
+        if (lb) {
+            if (mode == 0 && dump) RQ_SMALL(true, 0, true);
+            else if (mode == 0) RQ_SMALL(true, 0, false);
+            else if (mode == 1) RQ_SMALL(true, 1, false);
+            else RQ_SMALL(true, 2, false);
+        } else {
+            if (mode == 0 && dump) RQ_SMALL(false, 0, true);
+            else if (mode == 0) RQ_SMALL(false, 0, false);
+            else if (mode == 1) RQ_SMALL(false, 1, false);
+            else RQ_SMALL(false, 2, false);
+        }
+#undef RQ_SMALL
         RQ_CHECK_LAUNCH();
         return;
     }
-    const SmemPlan plan = smem_plan(a.Dp, ta, a.ngmax, a.minst);
+    const SmemPlan plan = smem_plan(a.Dp, ta);
     RQ_REQUIRE(plan.slots >= 2 && plan.total <= (uint32_t)kSmemLimit, RABITQ_ERR_INTERNAL,
                "grouped scan: TMEM / shared-memory plan does not fit");
     const size_t smem = plan.total;

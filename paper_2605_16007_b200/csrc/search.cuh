@@ -14,6 +14,16 @@ struct ColC {      // per grouped row (query, list) constants of the grouped sca
     int pair;      // (query, probe) pair index
 };
 
+// Column constants of the grouped scan as stored (global and shared memory):
+// two grouped rows per 64-byte record, so that the fast test of columns 2p,
+// 2p + 1 takes (-a, b) and (-K, U) of both with two 16-byte loads, already
+// paired for the packed FP32 ops (FFMA2 / FADD2)
+struct ColPair {
+    float na[2], b[2], nK[2], U[2];
+    float nq2[2], tau[2];
+    int q[2], pair[2];
+};
+
 struct ScanArgs {
     const int32_t* probes;     // [npairs] list of each (q, probe) pair
     int64_t npairs;
@@ -41,16 +51,17 @@ struct ScanArgs {
     // grouped tcgen05 path (scan_imma.cu)
     int nlist;
     int Dp;                    // D rounded up to 32 (K of the int8 MMA)
-    const int64_t* gstart;     // [nlist + 1] first grouped row of each list's pairs
+    const int64_t* gstart;     // [nlist + 1] first grouped row of each list's pairs (multiple of 16)
+    const int64_t* gcount;     // [nlist] grouped rows of each list (its region is rounded up to 16 rows)
+    int64_t nrows;             // grouped rows allocated (qbar8 / gpair / column constants)
     const int32_t* gpair;      // [npairs] pair index of each grouped row
     const uint8_t* qbar8;      // [(npairs + 128) x Dp] quantized queries, grouped by list
     const int64_t* list_items; // [nlist + 1] prefix of (128-vector tile, 128-query group) items
     const uint16_t* pcnt;      // [nslots] popcount of each code
     const uint8_t* codes8;     // [nslots + 128][Dp] expanded codes (nullable: expanded in the kernel)
     int64_t nslots;
-    const ColC* gcolc;         // [npairs] column constants in grouped order
+    const ColPair* gcolp;      // [nrows / 2] column constants in grouped order
     const float* list_amax;    // [nlist] max n_o^2 of each list (fast-test margin)
-    int experiment;            // diagnostics (RABITQ_IMMA_EXPERIMENT): 1 skip epilogue math, 2 skip UMMAs
     long long* trace;          // diagnostics (RABITQ_SCAN_TRACE): clock64 stamps of CTA 0, [trace_n][16]
     int trace_n;
     // dense key dump (threshold-seeding sample scan): key of every scanned pair
@@ -59,8 +70,8 @@ struct ScanArgs {
     const int64_t* dense_base;  // [nq] first key of each query
     const int64_t* dense_off;   // [npairs] offset of each (query, probe) pair within its query
     int full;                   // 1: unquantized query (NEXT-1), 4 digit rows per pair (npairs = rows)
-    int ngmax;                  // TMA-A scan: largest group (set by scan_imma)
-    int minst;                  // TMA-A scan: fewest A stages (set by scan_imma)
+    int small;                  // 1: Dp <= 128 may take the small-K scan (scan_small_kernel)
+    int64_t items_bound;        // upper bound on the grouping's work items (small-K item table)
 };
 
 template <typename T>
@@ -82,20 +93,19 @@ struct Groups {
     WBuf<int32_t> gfill, gpos, gpair;
     WBuf<uint8_t> qbar8;
     int Dp = 0;
+    int64_t nrows = 0;  // grouped rows allocated (each list's region padded to 16 rows)
+    bool ta = false;    // A operand = the index's expanded codes by TMA (else expanded in the kernel)
     int64_t n = 0;  // grouped pairs
     int rows = 1;   // B rows per pair (4: the unquantized query's digit rows, NEXT-1)
 };
 void prepare_groups(const rabitq_index* idx, const int32_t* probes, int64_t n, const int32_t* sub, Groups& g,
-                    cudaStream_t st, int& launches, int rows = 1);
+                    cudaStream_t st, int& launches, int rows, bool ta);
 int64_t regroup_flagged(const rabitq_index* idx, const int32_t* probes, int64_t npairs, int nprobe, const int* flags,
                         int max_rank, const Groups& full, Groups& sub, cudaStream_t st, int& launches);
 bool imma_wanted(const rabitq_index* idx, int64_t npairs, int scan_path);
+int64_t item_bound(const rabitq_index* idx, int64_t rows, int64_t max_group);
 // build time: idx->codes8 (the grouped scan's A operand, loaded by TMA) when it fits
 void expand_codes(rabitq_index* idx, cudaStream_t st);
-// the expanded codes the grouped scan uses (nullptr: in-kernel expansion)
-const uint8_t* codes8_of(const rabitq_index* idx);
-int ta_ngmax();
-int ta_minstages();
 cudaStream_t side_stream(const rabitq_index* idx);
 
 struct RerankArgs {
@@ -133,13 +143,6 @@ struct RerankArgs {
     // bound-driven re-rank set (NEXT-4): keep est - bound <= k-th smallest est + bound
     int adaptive;
     unsigned long long* reranked;  // [1] candidates kept, summed over queries (adaptive only)
-    // split re-rank (select_rerank_kernel<2> + rr_gather / rr_filter / rr_final):
-    // per (query, candidate i) scratch at q Mp + i and the exact-distance task list
-    uint64_t* dk_g;                // [nq x Mp] (d or d~ + delta, row) keys
-    float* lowb_g;                 // [nq x Mp] d~ - delta (dense candidates), +inf otherwise
-    int* m_g;                      // [nq] candidates of each query
-    uint2* tasks;                  // {q Mp + i, row}
-    unsigned int* ntask;           // [1]
 };
 
 struct SearchCfg {
@@ -151,6 +154,7 @@ struct SearchCfg {
     int refine_rank = 0;  // > 0: refine tau with a tensor-core pass over each query's nearest lists
     int rerank = 0;       // 1: bound-driven re-rank set (NEXT-4)
     int full = 0;         // 1: unquantized query (NEXT-1), grouped tensor-core scan
+    uint32_t variant = 0; // result-invariant execution variants (rabitq_search_opts.variant)
 };
 
 struct DebugOut {  // device-or-host pointers (cudaMemcpyDefault), all nullable

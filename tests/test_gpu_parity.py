@@ -60,7 +60,7 @@ def debug_search(idx, Q, k, nprobe, M, dump=True, **kw):
     if dump:
         cap = nq * nprobe * ((info["max_list"] + 31) // 32) * 32
         dbg["scan_ip"] = torch.full((cap,), -1, dtype=torch.int32, device=dev)
-        dbg["scan_est"] = torch.empty(cap, device=dev)
+        dbg["scan_est"] = torch.zeros(cap, device=dev)  # pad slots are never written
         dbg["scan_dump_cap"] = cap
     ids, d = idx.search(Q.cuda(), k, nprobe, M, debug=dbg, **kw)
     torch.cuda.synchronize()
@@ -203,7 +203,7 @@ def test_stage_parity(orc, D, N, nlist, nq, nprobe, k, M, scan_path):
 
 
 @pytest.mark.parametrize("nlist,nprobe,nq", [(2048, 300, 40), (4096, 64, 300), (16384, 128, 64)])
-def test_probe_select_large_nlist(nlist, nprobe, nq, monkeypatch):
+def test_probe_select_large_nlist(nlist, nprobe, nq):
     """Probe lists at large nlist (sampled-threshold select, search.cu
     probe_select_big_kernel): the oracle's ranking of the GPU's own q' (L1),
     and bit-identical to the radix select over the whole row."""
@@ -211,8 +211,7 @@ def test_probe_select_large_nlist(nlist, nprobe, nq, monkeypatch):
     idx = build(X, nlist)
     _, _, a = debug_search(idx, Q, 10, nprobe, 50, dump=False)
     pu.check_probe_lists(a["probes"], a["qrot"], idx.export()["centroids"], nprobe)
-    monkeypatch.setenv("RABITQ_PROBE_SELECT", "radix")
-    _, _, b = debug_search(idx, Q, 10, nprobe, 50, dump=False)
+    _, _, b = debug_search(idx, Q, 10, nprobe, 50, dump=False, variant=rq.VARIANT_RADIX_PROBE)
     assert np.array_equal(a["probes"], b["probes"])
 
 
@@ -235,7 +234,7 @@ def test_scan_paths_identical(D):
 
 
 @pytest.mark.parametrize("D", [96, 960])
-def test_scan_code_operand_paths_identical(D, monkeypatch):
+def test_scan_code_operand_paths_identical(D):
     """The grouped scan's A operand from the expanded codes in HBM (TMA) and
     from the in-kernel expansion into TMEM (index built without the expanded
     copy) give bit-identical results, including the debug dump of every ip and
@@ -245,14 +244,12 @@ def test_scan_code_operand_paths_identical(D, monkeypatch):
     assert a.info()["bytes_codes8"] > 0
     ai, ad, adbg = debug_search(a, Q[:64], 10, 8, 200, scan_path=rq.SCAN_IMMA)
     si, sd = a.search(Q.cuda(), 10, 8, 200, scan_path=rq.SCAN_IMMA)
-    monkeypatch.setenv("RABITQ_CODES8", "0")  # the same index, codes expanded in the kernel
-    bi, bd, bdbg = debug_search(a, Q[:64], 10, 8, 200, scan_path=rq.SCAN_IMMA)
-    ti, td = a.search(Q.cuda(), 10, 8, 200, scan_path=rq.SCAN_IMMA)
+    # the same index, codes expanded in the kernel
+    bi, bd, bdbg = debug_search(a, Q[:64], 10, 8, 200, scan_path=rq.SCAN_IMMA, variant=rq.VARIANT_EXPAND_IN_KERNEL)
+    ti, td = a.search(Q.cuda(), 10, 8, 200, scan_path=rq.SCAN_IMMA, variant=rq.VARIANT_EXPAND_IN_KERNEL)
     assert np.array_equal(ai, bi) and np.array_equal(ad, bd)
     assert np.array_equal(adbg["scan_ip"], bdbg["scan_ip"]) and np.array_equal(adbg["scan_est"], bdbg["scan_est"])
     assert torch.equal(si, ti) and torch.equal(sd, td)
-    b = build(X, 32)  # built without the expanded copy
-    assert b.info()["bytes_codes8"] == 0
 
 
 @pytest.mark.parametrize("D,M", [(128, 100), (960, 400)])
@@ -347,22 +344,27 @@ def test_fullq_parity(orc, D, N, nlist, nq, nprobe, k, M):
     pu.check_final(ids, d, ri, rd, k)
 
 
-@pytest.mark.parametrize("D", [128, 960])
-def test_split_rerank_identical(D, monkeypatch):
-    """The split re-rank path (select -> persistent gather -> dense filter ->
-    gather -> top-k, RABITQ_RR_SPLIT=1) returns exactly the fused kernel's ids
-    and distances (same candidates, same exact-distance arithmetic), with and
-    without the dense nearest-list block (>= 256 queries)."""
-    X, Q = make_data(D, 40000 if D < 900 else 8000, 32, 300)
-    idx = build(X, 32)
-    a_i, a_d = idx.search(Q.cuda(), 10, 8, 200)
-    monkeypatch.setenv("RABITQ_RR_SPLIT", "1")
-    b_i, b_d = idx.search(Q.cuda(), 10, 8, 200)
-    c_i, c_d = idx.search(Q[:100].cuda(), 10, 8, 200)  # < 256 queries: no dense block
-    monkeypatch.delenv("RABITQ_RR_SPLIT")
-    e_i, e_d = idx.search(Q[:100].cuda(), 10, 8, 200)
-    assert torch.equal(a_i, b_i) and torch.equal(a_d, b_d)
-    assert torch.equal(c_i, e_i) and torch.equal(c_d, e_d)
+@pytest.mark.parametrize("D,N,nlist,nq", [(128, 40000, 32, 300), (96, 60000, 24, 700), (33, 20000, 16, 200)])
+def test_small_scan_identical(D, N, nlist, nq):
+    """d <= 128: the small-K grouped scan (tiles dealt to 4 epilogue warpgroups,
+    TMEM accumulator ring, dynamic item scheduler) and the generic grouped
+    scan give bit-identical stage outputs: threshold, survivor counts, top-M
+    ids and estimates, every dumped ip / estimate, final ids and distances,
+    with several query groups per list (nq * nprobe / nlist > 256) and ragged
+    Dp (33 -> 64)."""
+    X, Q = make_data(D, N, nlist, nq)
+    idx = build(X, nlist)
+    nprobe = 12 if nlist >= 24 else 8
+    a = debug_search(idx, Q, 10, nprobe, 200, scan_path=rq.SCAN_IMMA)
+    b = debug_search(idx, Q, 10, nprobe, 200, scan_path=rq.SCAN_IMMA, variant=rq.VARIANT_GENERIC_SCAN)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    for key in ("tau", "survivors", "topm_ids", "topm_est", "scan_ip", "scan_est"):
+        assert np.array_equal(a[2][key], b[2][key]), key
+    # without the dump (the packed fast survivor test) and with the lower-bound key
+    for kw in (dict(), dict(rank_key=rq.RANK_LOWER_BOUND)):
+        si, sd = idx.search(Q.cuda(), 10, nprobe, 200, scan_path=rq.SCAN_IMMA, **kw)
+        gi, gd = idx.search(Q.cuda(), 10, nprobe, 200, scan_path=rq.SCAN_IMMA, variant=rq.VARIANT_GENERIC_SCAN, **kw)
+        assert torch.equal(si, gi) and torch.equal(sd, gd)
 
 
 def test_scan_paths_identical_multigroup_d960():
@@ -373,18 +375,6 @@ def test_scan_paths_identical_multigroup_d960():
     idx = build(X, 8)
     a_i, a_d = idx.search(Q.cuda(), 10, 4, 300, scan_path=rq.SCAN_POPC)
     b_i, b_d = idx.search(Q.cuda(), 10, 4, 300, scan_path=rq.SCAN_IMMA)
-    assert torch.equal(a_i, b_i) and torch.equal(a_d, b_d)
-
-
-@pytest.mark.parametrize("D", [96, 960])
-def test_swapped_scan_identical(D, monkeypatch):
-    """The operand-swapped main scan (RABITQ_SWAP=1: queries resident in TMEM,
-    code tiles streamed) returns exactly the default kernel's results."""
-    X, Q = make_data(D, 40000 if D < 900 else 8000, 32, 300)
-    idx = build(X, 32)
-    a_i, a_d = idx.search(Q.cuda(), 10, 8, 200, scan_path=rq.SCAN_IMMA)
-    monkeypatch.setenv("RABITQ_SWAP", "1")
-    b_i, b_d = idx.search(Q.cuda(), 10, 8, 200, scan_path=rq.SCAN_IMMA)
     assert torch.equal(a_i, b_i) and torch.equal(a_d, b_d)
 
 
