@@ -162,6 +162,15 @@ typedef struct {
     uint32_t variant;        /* 0 (default) or an OR of RABITQ_VARIANT_*: alternative execution
                                 paths of the same computation (parity tests prove them
                                 bit-identical to the default); never changes results        */
+    const int32_t* probes_in;/* nullable [nq x nprobe] (host or device): the probed lists of each
+                                query, e.g. from rabitq_probe; stage S2-S3 is
+                                skipped.  Ids outside [0, nlist) -> INVALID_ARGUMENT.  Results
+                                equal the default search when these are rabitq_probe's lists */
+    int32_t query_split;     /* rabitq_search_sharded only: 0 every rank probes every query;
+                                1 rank g probes queries [g c, (g+1) c), c = ceil(nq / G), and
+                                the probe lists are all-gathered (one ncclAllGather of
+                                nq x nprobe int32) -- the probe GEMM is split G ways
+                                (SURVEY 8(e)); results are identical                          */
 } rabitq_search_opts;
 
 /* rabitq_search_opts.variant bits (results are identical with any of them) */
@@ -187,6 +196,15 @@ rabitq_status rabitq_search_ex(const rabitq_index* idx, const float* Q, int64_t 
                                int32_t nprobe, int32_t n_rerank, const rabitq_search_opts* opts,
                                int64_t* ids, float* dists);
 void rabitq_search_opts_default(rabitq_search_opts* opts);
+
+/* Stages S1-S3 only: rotate Q [nq x d] and
+ * write each query's nprobe nearest lists, ascending by (distance, list id),
+ * to probes [nq x nprobe] int32 (host or device).  stream: cudaStream_t or NULL
+ * (the index's stream); synchronous w.r.t. host buffers.  nprobe = 0 means AUTO.
+ * Errors: nprobe > nlist, nq < 0 -> INVALID_ARGUMENT; non-finite Q ->
+ * INVALID_DATA. */
+rabitq_status rabitq_probe(const rabitq_index* idx, const float* Q, int64_t nq, int32_t nprobe, int32_t* probes,
+                           void* stream);
 
 /* ----------------------------------------------------- info / export -- */
 typedef struct {

@@ -103,6 +103,8 @@ class SearchOpts(ctypes.Structure):
         ("rerank", ctypes.c_int32),
         ("query_bits", ctypes.c_int32),
         ("variant", ctypes.c_uint32),
+        ("probes_in", ctypes.c_void_p),
+        ("query_split", ctypes.c_int32),
     ]
 
 
@@ -128,7 +130,7 @@ EXPORTED = [
     "rabitq_build", "rabitq_build_ex", "rabitq_build_opts_default", "rabitq_search", "rabitq_search_ex",
     "rabitq_search_opts_default", "rabitq_index_info", "rabitq_index_export", "rabitq_free",
     "rabitq_last_error", "rabitq_version", "rabitq_comm_unique_id", "rabitq_comm_init", "rabitq_comm_free",
-    "rabitq_search_sharded", "rabitq_merge_topk", "rabitq_selftest",
+    "rabitq_search_sharded", "rabitq_merge_topk", "rabitq_selftest", "rabitq_probe",
 ]
 
 _lib = None
@@ -247,7 +249,7 @@ class Index:
                rank_key: int = RANK_EST, eps0: float = 0.0, query_id_base: int = 0, cap: int = 0,
                seed_max: int = 0, stream=None, debug: Optional[dict] = None, out=None,
                profile: Optional[Profile] = None, rerank: int = RERANK_FIXED, query_bits: int = 4,
-               variant: int = 0):
+               variant: int = 0, probes=None):
         """Returns (ids int64 [nq, k], dists float32 [nq, k]) on Q's device.
         ``debug`` maps rabitq_debug member names to preallocated tensors.
         Device inputs run on ``stream`` (default: torch's current stream)."""
@@ -269,6 +271,9 @@ class Index:
         o.rerank = rerank
         o.query_bits = query_bits
         o.variant = variant
+        if probes is not None:
+            probes = probes.contiguous() if hasattr(probes, "contiguous") else np.ascontiguousarray(probes, np.int32)
+            o.probes_in = _ptr(probes)
         o.stream = _call_stream(stream, Q, temps)
         dbg = None
         if debug:
@@ -285,6 +290,19 @@ class Index:
                                       ctypes.c_int32(nprobe), ctypes.c_int32(n_rerank), ctypes.byref(o),
                                       ctypes.c_void_p(_ptr(ids)), ctypes.c_void_p(_ptr(dists))))
         return ids, dists
+
+    # -- rabitq_probe (S1-S3 only) ----------------------------------------------
+    def probe(self, Q, nprobe: int, *, stream=None):
+        """int32 [nq, nprobe]: each query's nearest lists, ascending (d, list)."""
+        torch = _torch()
+        Q0 = Q
+        Q = _as_f32(Q)
+        nq = Q.shape[0]
+        out = torch.empty((nq, nprobe), dtype=torch.int32, device=Q.device)
+        h = _call_stream(stream, Q, [Q if Q is not Q0 else None, out])
+        _check(lib().rabitq_probe(self._h, ctypes.c_void_p(_ptr(Q)), ctypes.c_int64(nq), ctypes.c_int32(nprobe),
+                                  ctypes.c_void_p(_ptr(out)), ctypes.c_void_p(h)))
+        return out
 
     def info(self) -> dict:
         i = IndexInfo()

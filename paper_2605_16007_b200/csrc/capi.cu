@@ -294,9 +294,18 @@ static void search_local(const rabitq_index* idx, const float* Q, int64_t nq, in
             v_sest.init(dg->scan_est, (size_t)dg->scan_dump_cap, idx->device, st);
         }
     }
+    // caller's probe lists (query-split probing): staged on the device once
+    const bool pin_dev = o.probes_in && on_device(o.probes_in, idx->device);
+    Stage sp(o.probes_in && !pin_dev ? (size_t)nq * nprobe * sizeof(int32_t) : 0, st);
+    const int32_t* probes_d = o.probes_in;
+    if (o.probes_in && !pin_dev) {
+        RQ_CUDA(cudaMemcpyAsync(sp.p, o.probes_in, (size_t)nq * nprobe * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        probes_d = (const int32_t*)sp.p;
+    }
     rabitq::SearchStats stats;
     stats.timing = o.profile != nullptr;
     for (int64_t b0 = 0; b0 < nq; b0 += qbatch) {
+        cfg.probes_in = probes_d ? probes_d + (size_t)b0 * nprobe : nullptr;
         const int64_t m = std::min(qbatch, nq - b0);
         rabitq::DebugOut dbg;
         if (dg) {
@@ -451,6 +460,34 @@ rabitq_status rabitq_index_export(const rabitq_index* idx, rabitq_export_t* out)
     API_END
 }
 
+rabitq_status rabitq_probe(const rabitq_index* idx, const float* Q, int64_t nq, int32_t nprobe, int32_t* probes,
+                           void* stream) {
+    API_BEGIN
+    RQ_REQUIRE(idx != nullptr, RABITQ_ERR_INVALID_ARGUMENT, "index is NULL");
+    RQ_REQUIRE(nq >= 0 && nprobe >= 0, RABITQ_ERR_INVALID_ARGUMENT, "nq < 0 or nprobe < 0");
+    if (nprobe == 0) nprobe = std::max(1, (int)std::ceil(0.05 * idx->nlist));  // AUTO
+    RQ_REQUIRE(nprobe <= idx->nlist, RABITQ_ERR_INVALID_ARGUMENT, "nprobe > nlist");
+    if (nq == 0) return RABITQ_OK;
+    RQ_REQUIRE(Q && probes, RABITQ_ERR_INVALID_ARGUMENT, "Q / probes is NULL");
+    RQ_CUDA(cudaSetDevice(idx->device));
+    cudaStream_t st = stream ? (cudaStream_t)stream : idx->stream;
+    const int D = idx->D;
+    const bool q_dev = on_device(Q, idx->device), p_dev = on_device(probes, idx->device);
+    Stage sq(q_dev ? 0 : (size_t)nq * D * 4, st), sp(p_dev ? 0 : (size_t)nq * nprobe * 4, st);
+    const float* Qd = Q;
+    if (!q_dev) {
+        RQ_CUDA(cudaMemcpyAsync(sq.p, Q, (size_t)nq * D * 4, cudaMemcpyHostToDevice, st));
+        Qd = (const float*)sq.p;
+    }
+    int32_t* pd = p_dev ? probes : (int32_t*)sp.p;
+    rabitq::probe_only(idx, Qd, nq, nprobe, 0, pd, st);
+    if (!p_dev) {
+        RQ_CUDA(cudaMemcpyAsync(probes, pd, (size_t)nq * nprobe * 4, cudaMemcpyDeviceToHost, st));
+        RQ_CUDA(cudaStreamSynchronize(st));
+    }
+    API_END
+}
+
 // ------------------------------------------------------------ multi-GPU --
 rabitq_status rabitq_comm_unique_id(uint8_t uid[128]) {
     API_BEGIN
@@ -512,6 +549,19 @@ rabitq_status rabitq_search_sharded(const rabitq_index* shard, rabitq_comm* comm
     }
     const size_t nk = (size_t)nq * k;
     Stage li(nk * 8, st), ld(nk * 4, st), gi(nk * G * 8, st), gd(nk * G * 4, st), oi(nk * 8, st), od(nk * 4, st);
+    Stage pr, pg;
+    if (o.query_split && G > 1 && !o.probes_in) {
+        // query-split probing: rank g probes its c = ceil(nq / G)
+        // queries, then one all-gather of the [G c x nprobe] probe lists
+        const int64_t c = (nq + G - 1) / G, lo = std::min<int64_t>(nq, (int64_t)comm->rank * c);
+        const int64_t m = std::min<int64_t>(c, nq - lo);
+        pr = Stage((size_t)c * nprobe * sizeof(int32_t), st);
+        pg = Stage((size_t)G * c * nprobe * sizeof(int32_t), st);
+        if (m > 0) rabitq::probe_only(shard, Qd + (size_t)lo * D, m, nprobe, o.variant, (int32_t*)pr.p, st);
+        ncclResult_t r = ncclAllGather(pr.p, pg.p, (size_t)c * nprobe, ncclInt32, comm->comm, st);
+        RQ_REQUIRE(r == ncclSuccess, RABITQ_ERR_NCCL, std::string("ncclAllGather (probes): ") + ncclGetErrorString(r));
+        o.probes_in = (const int32_t*)pg.p;
+    }
     search_local(shard, Q, nq, k, nprobe, n_rerank, o, (int64_t*)li.p, (float*)ld.p, st, Qd);
     // the one exchange step: all-gather of the per-rank top-k over NVLink
     ncclResult_t r = ncclGroupStart();

@@ -786,9 +786,10 @@ __global__ void expand_codes_kernel(const uint32_t* __restrict__ codes, int64_t 
 // samples on the per-tile row loads, 7 % on the tail, 8 % of the
 // instructions in decode_item's binary search).  Here:
 //  * the unit of epilogue work is (tile, block of <= 64 group columns): one
-//    of 8 TMEM accumulator slots of 64 columns; units are dealt round-robin
-//    to 4 epilogue warpgroups (4 warps = the 4 TMEM lane quarters), so up to
-//    8 units are in flight and a wide group keeps every warpgroup busy;
+//    of 8 TMEM accumulator slots of 64 columns, up to 8 units in flight; each
+//    of the 24 epilogue warps takes the next unit of its TMEM lane quarter
+//    from a shared counter (6 warps per quarter), so a wide group keeps every
+//    warp busy and a slow unit does not stall the others;
 //  * the unit's per-vector constants (n_o^2 and f, popcount, row id, g1) are
 //    staged in shared memory by bulk copies next to the accumulator slot;
 //  * items (list, group of <= 256 queries, <= 8 tiles) come from a table
@@ -804,12 +805,12 @@ constexpr int kSkRI = 6;                                     // item ring
 constexpr int kSkSA = 5;                                     // A stages (16 KB)
 constexpr int kSkUS = kTmemCols / kSkUW;                     // 8 units in flight
 constexpr int kSkEpi0 = 3;                                   // warps 0 sched + B, 1 A + row constants, 2 MMA
-constexpr int kSkNT = (kSkEpi0 + kEpiWarps) * 32;            // 608 threads
+constexpr int kSkEpiW = 24;                                  // epilogue warps (6 per TMEM lane quarter)
+constexpr int kSkNT = (kSkEpi0 + kSkEpiW) * 32;              // 864 threads (72 registers)
 constexpr uint32_t kSkBStage = kSkNG * kKC;                  // 32 KB
 constexpr uint32_t kSkCStage = kSkNG / 2 * sizeof(ColPair);  // 8 KB
 struct SkRows {                                              // one unit's per-vector constants
     float2 fac[kTM];
-    float g1[kTM];
     uint32_t rows[kTM];
     uint16_t pcnt[kTM];
 };
@@ -859,6 +860,7 @@ __global__ __launch_bounds__(kSkNT, 1) void scan_small_kernel(const __grid_const
     ColPair* colc = reinterpret_cast<ColPair*>(smem + kSkOffC);
     SkRows* urows = reinterpret_cast<SkRows*>(smem + kSkOffR);
     __shared__ int4 rec[kSkRI];
+    __shared__ uint32_t next_unit[4];  // epilogue: next unit of each TMEM lane quarter
     __shared__ __align__(8) uint64_t ifull[kSkRI], iempty[kSkRI], bfull[2], bfree[2], afull[kSkSA], aempty[kSkSA],
         accf[kSkUS], acce[kSkUS], rowf[kSkUS];
     __shared__ uint32_t tmem_base_s;
@@ -867,7 +869,7 @@ __global__ __launch_bounds__(kSkNT, 1) void scan_small_kernel(const __grid_const
     if (tid == 0) {
         for (int s = 0; s < kSkRI; ++s) {
             tc::mbar_init(&ifull[s], 1);
-            tc::mbar_init(&iempty[s], 2 + kEpiWarps);  // A loader, MMA warp, every epilogue warp
+            tc::mbar_init(&iempty[s], 2 + kSkEpiW);  // A loader, MMA warp, every epilogue warp
         }
         for (int b = 0; b < 2; ++b) {
             tc::mbar_init(&bfull[b], 1);
@@ -882,6 +884,7 @@ __global__ __launch_bounds__(kSkNT, 1) void scan_small_kernel(const __grid_const
             tc::mbar_init(&acce[k], 4);  // the 4 warps of the unit's warpgroup
             tc::mbar_init(&rowf[k], 1);
         }
+        for (int q = 0; q < 4; ++q) next_unit[q] = 0u;
         tc::prefetch_tmap(&tmapB);
         tc::prefetch_tmap(&tmapA);
     }
@@ -919,7 +922,7 @@ __global__ __launch_bounds__(kSkNT, 1) void scan_small_kernel(const __grid_const
             }
         }
     } else if (warp == 1) {
-        // ============ code operand (A) by TMA, per-vector constants by bulk copies ============
+        // ============ code operand (A) by TMA ============
         if (lane == 0) {
             uint32_t tcnt = 0, ucnt = 0;
             for (uint32_t i = 0;; ++i) {
@@ -928,14 +931,17 @@ __global__ __launch_bounds__(kSkNT, 1) void scan_small_kernel(const __grid_const
                 const int4 r = rec[s];
                 tc::mbar_arrive(&iempty[s]);
                 if (r.w == 0) break;
-                const int nc = r.w & 511, nt = (r.w >> 9) & 15, t0 = (int)((uint32_t)r.w >> 13);
-                const int nu = (nc + kSkUW - 1) / kSkUW;
+                const int nt = (r.w >> 9) & 15, t0 = (int)((uint32_t)r.w >> 13);
+                const int nu = ((r.w & 511) + kSkUW - 1) / kSkUW;
                 for (int t = 0; t < nt; ++t, ++tcnt) {
                     const int st = (int)(tcnt % kSkSA);
                     if (tcnt >= (uint32_t)kSkSA) tc::mbar_wait(&aempty[st], ((tcnt / kSkSA) - 1) & 1);
                     tc::mbar_arrive_expect_tx(&afull[st], (uint32_t)kAStage);
+                    tc::tma_load_2d(smem + kSkOffA + st * kAStage, &tmapA, &afull[st], 0, r.x + (t0 + t) * kTM);
+                    // the tile's per-vector constants, once per unit, as each unit slot frees up
+                    // (issued right behind the tile's code operand: measured faster than a
+                    // separate loader warp, whose copies queue behind code tiles issued ahead)
                     const int v0 = (t0 + t) * kTM;
-                    tc::tma_load_2d(smem + kSkOffA + st * kAStage, &tmapA, &afull[st], 0, r.x + v0);
                     const int nv = r.y - v0 < kTM ? r.y - v0 : kTM;
                     const uint32_t ncp = (uint32_t)((nv + 31) & ~31);  // whole 32-slot blocks of the list
                     const int64_t s0 = (int64_t)r.x + v0;
@@ -943,11 +949,10 @@ __global__ __launch_bounds__(kSkNT, 1) void scan_small_kernel(const __grid_const
                         const int k = (int)(ucnt % kSkUS);
                         if (ucnt >= (uint32_t)kSkUS) tc::mbar_wait(&acce[k], ((ucnt / kSkUS) - 1) & 1);
                         SkRows& R = urows[k];
-                        tc::mbar_arrive_expect_tx(&rowf[k], ncp * ((kLB ? 18u : 14u)));
+                        tc::mbar_arrive_expect_tx(&rowf[k], ncp * 14u);
                         tc::bulk_load(R.fac, a.fac + s0, ncp * 8u, &rowf[k]);
                         tc::bulk_load(R.pcnt, a.pcnt + s0, ncp * 2u, &rowf[k]);
                         tc::bulk_load(R.rows, a.rows + s0, ncp * 4u, &rowf[k]);
-                        if (kLB) tc::bulk_load(R.g1, a.g1 + s0, ncp * 4u, &rowf[k]);
                     }
                 }
             }
@@ -990,41 +995,69 @@ __global__ __launch_bounds__(kSkNT, 1) void scan_small_kernel(const __grid_const
                 if (t == nt - 1) tc::commit_warp(&bfree[b]);  // the item's query operand is free
             }
         }
-    } else {
-        // ============ epilogue: warpgroup (unit % 4), 32 rows x the unit's columns per warp ============
-        const int e = warp - kSkEpi0, wg = e >> 2, quarter = warp & 3;
+    } else if (warp >= kSkEpi0) {
+        // ============ epilogue: 32 rows (the warp's TMEM lane quarter) x a unit's columns ============
+        // Units are taken dynamically, per lane quarter: the 4 warps of quarter q
+        // share a counter, so a unit that takes long (many survivors) holds up
+        // neither the other quarters nor the other units; the MMA fills units in
+        // order and blocks only when it wraps around to a slot still in use.
+        const int quarter = warp & 3;
         const int r = quarter * 32 + lane;
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
-        uint32_t ucnt = 0;
-        for (uint32_t i = 0;; ++i) {
+        const uint32_t rowf_s = tc::smem_u32(rowf), accf_s = tc::smem_u32(accf), acce_s = tc::smem_u32(acce);
+        uint32_t i = 0, u0 = 0;  // item cursor and its first unit
+        int4 R = make_int4(0, 0, 0, 0);
+        int nu = 0, nut = -1;     // nut < 0: item i not read yet
+        for (;;) {
+            uint32_t uc = 0;
+            if (lane == 0) uc = atomicAdd(&next_unit[quarter], 1u);
+            uc = __shfl_sync(0xFFFFFFFFu, uc, 0);
+            bool done = false;
+            for (;;) {  // advance to the item holding unit uc, releasing the items passed
+                if (nut < 0) {
+                    tc::mbar_wait(&ifull[i % kSkRI], (i / kSkRI) & 1);
+                    R = rec[i % kSkRI];
+                    if (R.w == 0) {
+                        done = true;
+                        break;
+                    }
+                    nu = ((R.w & 511) + kSkUW - 1) / kSkUW;
+                    nut = ((R.w >> 9) & 15) * nu;
+                }
+                if (uc < u0 + (uint32_t)nut) break;
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&iempty[i % kSkRI]);
+                u0 += (uint32_t)nut;
+                ++i;
+                nut = -1;
+            }
+            if (done) break;
             const int s = (int)(i % kSkRI);
-            tc::mbar_wait(&ifull[s], (i / kSkRI) & 1);
-            const int4 R = rec[s];
-            if (R.w == 0) break;
-            const int nc = R.w & 511, nt = (R.w >> 9) & 15, t0 = (int)((uint32_t)R.w >> 13);
-            const int nu = (nc + kSkUW - 1) / kSkUW;
-            for (int t = 0; t < nt; ++t) {
-                const int64_t v = (int64_t)(t0 + t) * kTM + r;
-                const bool vok = v < R.y;
-                for (int u = 0; u < nu; ++u, ++ucnt) {
-                    if ((int)(ucnt & 3u) != wg) continue;
-                    const int k = (int)(ucnt % kSkUS);
-                    const uint32_t ph = (ucnt / kSkUS) & 1;
+            const int nc = R.w & 511, t0 = (int)((uint32_t)R.w >> 13);
+            const int x = (int)(uc - u0);
+            const int t = nu == 1 ? x : x / nu, u = x - t * nu;
+            const int64_t v = (int64_t)(t0 + t) * kTM + r;
+            const bool vok = v < R.y;
+            {
+                {
+                    const int k = (int)(uc % kSkUS);
+                    const uint32_t ph = (uc / kSkUS) & 1;
                     const ColPair* cb = colc + s * (kSkNG / 2) + u * (kSkUW / 2);
                     const int w = nc - u * kSkUW < kSkUW ? nc - u * kSkUW : kSkUW;
-                    tc::mbar_wait(&rowf[k], ph);
+                    tc::mbar_wait_s(rowf_s + 8u * k, ph);
                     const SkRows& RS = urows[k];
                     const float2 fac = vok ? RS.fac[r] : make_float2(0.f, 0.f);
                     const float pcf = vok ? (float)RS.pcnt[r] : 0.f;
-                    const float g1 = (kLB && vok) ? RS.g1[r] : 0.f;
+                    const float g1 = (kLB && vok) ? __ldg(a.g1 + R.x + v) : 0.f;  // lower-bound key only
                     const uint32_t row = vok ? RS.rows[r] : 0u;
-                    tc::mbar_wait(&accf[k], ph);
+                    tc::mbar_wait_s(accf_s + 8u * k, ph);
                     tc::fence_after_sync();
                     const uint32_t tbase = lane_base + (uint32_t)(k * kSkUW);
-                    uint32_t hc_cols[4], hc_bal[4];
-                    int hc_base[4];
+                    constexpr int kH = kSkUW / kEC;  // 16-column chunks per unit
+                    uint32_t hc_cols[kH], hc_bal[kH];
+                    int hc_base[kH];
 #pragma unroll
-                    for (int h = 0; h < 4; ++h) {
+                    for (int h = 0; h < kH; ++h) {
                         hc_cols[h] = 0u;
                         hc_bal[h] = 0u;
                         hc_base[h] = 0;
@@ -1117,7 +1150,7 @@ __global__ __launch_bounds__(kSkNT, 1) void scan_small_kernel(const __grid_const
                     if constexpr (kMode != 2) {
                         // survivors re-read their accumulator column and store (key, row)
 #pragma unroll
-                        for (int h = 0; h < 4; ++h) {
+                        for (int h = 0; h < kH; ++h) {
                             const uint32_t cols = hc_cols[h];
                             if (!cols) continue;
                             const int col0 = h * kEC;
@@ -1137,11 +1170,9 @@ __global__ __launch_bounds__(kSkNT, 1) void scan_small_kernel(const __grid_const
                     }
                     tc::fence_before_sync();
                     __syncwarp();
-                    if (lane == 0) tc::mbar_arrive(&acce[k]);  // the slot (accumulator + rows) may be reused
+                    if (lane == 0) tc::mbar_arrive_s(acce_s + 8u * k);  // the slot (accumulator + rows) may be reused
                 }
             }
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&iempty[s]);
         }
     }
     tc::fence_before_sync();

@@ -155,6 +155,7 @@ struct SearchCfg {
     int rerank = 0;       // 1: bound-driven re-rank set (NEXT-4)
     int full = 0;         // 1: unquantized query (NEXT-1), grouped tensor-core scan
     uint32_t variant = 0; // result-invariant execution variants (rabitq_search_opts.variant)
+    const int32_t* probes_in = nullptr;  // DEVICE [nq x nprobe]: skip S2-S3 (query-split probing)
 };
 
 struct DebugOut {  // device-or-host pointers (cudaMemcpyDefault), all nullable
@@ -185,6 +186,34 @@ struct SearchStats {
     int batches = 0;
 };
 
+// per-stage CUDA events on the call's stream (rabitq_profile)
+struct StageTimer {
+    cudaEvent_t ev[9] = {};
+    bool on = false;
+    cudaStream_t st = nullptr;
+    StageTimer(bool enable, cudaStream_t s) : on(enable), st(s) {
+        if (on)
+            for (auto& e : ev) RQ_CUDA(cudaEventCreate(&e));
+    }
+    void mark(int i) {
+        if (on) RQ_CUDA(cudaEventRecord(ev[i], st));
+    }
+    void accumulate(float* ms) {
+        if (!on) return;
+        RQ_CUDA(cudaEventSynchronize(ev[8]));
+        for (int i = 0; i < 8; ++i) {
+            float t = 0.0f;
+            RQ_CUDA(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
+            ms[i] += t;
+        }
+    }
+    ~StageTimer() {
+        if (on)
+            for (auto& e : ev) cudaEventDestroy(e);
+    }
+};
+void rotate_probe(const rabitq_index* idx, const float* Q, int64_t nq, int nprobe, uint32_t variant, float* Qr,
+                  int32_t* probes, cudaStream_t st, int& L, StageTimer* tm);
 void search_batch(const rabitq_index* idx, const float* Q, int64_t nq, int k, int nprobe, int M,
                   const SearchCfg& cfg, int64_t qid_base, int64_t* ids, float* dists, const DebugOut& dbg,
                   cudaStream_t st, SearchStats* stats);
@@ -194,6 +223,8 @@ void group_items(const rabitq_index* idx, const int64_t* list_off, const Groups&
                  WBuf<int64_t>& items, cudaStream_t st, int& launches);
 uint64_t selftest_div(uint64_t n, uint64_t seed, cudaStream_t st);
 void scan_popc_entry(const ScanArgs& a, bool lb, bool retry, bool dump, cudaStream_t st);
+void probe_only(const rabitq_index* idx, const float* Q, int64_t nq, int nprobe, uint32_t variant, int32_t* probes,
+                cudaStream_t st);
 void merge_topk(const int64_t* in_ids, const float* in_d, int G, int64_t nq, int k, int64_t* out_ids,
                 float* out_d, cudaStream_t st);
 

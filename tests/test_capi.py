@@ -102,7 +102,7 @@ def _struct_fields(name):
     assert m, name
     names = []
     for decl in m.group(1).split(";"):
-        decl = decl.strip()
+        decl = re.sub(r"^const\s+", "", decl.strip())
         if not decl:
             continue
         head, _, rest = decl.partition(" ")

@@ -4,11 +4,16 @@ batch in one call), checked on sampled queries against the oracle run on a
 sub-index of the lists those queries probe (oracle/subindex.py):
 
   * L1  probe lists (GPU q' injected) identical up to near-ties
-  * L5  coarse top-M identical up to the estimator tie band
+  * L5  coarse top-M identical except ids within the two pairs' own estimator
+        tolerances of the oracle's M-th key (R#18)
   * L6  final top-k = the oracle's exact re-rank of the GPU's top-M
-  * end to end with the oracle's own rotation and probing: >= 75 % of the
-    sampled queries identical (the rest differ only through fp32-vs-fp64 ties)
-  * recall@k vs exact brute force (torch on the device) matches the oracle's
+  * end to end with the oracle's own fp64 rotation and probing: every query
+    that differs is explained -- its own probe lists differ from the GPU's
+    only by near-tied lists (L1), and with the GPU's q' injected the oracle
+    reproduces the GPU (L5/L6 above), so the difference is the 3xTF32
+    rotation's rounding (R#30) propagated through ties
+  * recall@k vs exact brute force: GPU and oracle on the same sample, their
+    difference bounded by the differing result slots
 
 CFG5 (1e9 x 96, 408 GB) does not fit one B200; DESIGN.md sec 8.
 """
@@ -44,16 +49,18 @@ def _free_gb():
     return f / 2 ** 30
 
 
-def _run(cfg, orc, nprobe=None):
+def _run(cfg, orc, nprobe=None, shard=None):
     s = synth.spec(cfg)
-    need = s.N * s.D * 4 / 2 ** 30 * 1.3 + 4
+    lo, hi = synth.shard_range(s.N, *shard) if shard else (0, s.N)
+    need = (hi - lo) * s.D * 4 / 2 ** 30 * 1.3 + 4
     if _free_gb() < need:
         pytest.skip(f"CFG{cfg} needs ~{need:.0f} GiB free")
     dev = torch.device("cuda", 0)
     cen = synth.centres(s, dev)
-    X = synth.base_rows(s, 0, s.N, dev, cen=cen)
+    X = synth.base_rows(s, lo, hi, dev, cen=cen)
     Q = synth.queries(s, dev, cen=cen)
-    idx = rq.Index(X, nlist=s.nlist, seed=s.build_seed, borrow=True, init_centroids=synth.init_centroids(s, dev))
+    idx = rq.Index(X, nlist=s.nlist, seed=s.build_seed, borrow=True, init_centroids=synth.init_centroids(s, dev),
+                   id_offset=lo)
     nprobe = nprobe or s.nprobe
     nq, D = Q.shape
     dbg = dict(qrot=torch.empty(nq, D, device=dev), probes=torch.empty(nq, nprobe, dtype=torch.int32, device=dev),
@@ -74,19 +81,25 @@ def _run(cfg, orc, nprobe=None):
     lists = np.unique(np.concatenate([probes[sample].ravel(), own.ravel()]))
     from oracle.subindex import SubIndex
 
-    sub = SubIndex(ex, lists, lambda gids: X[torch.from_numpy(gids).to(dev)].cpu().numpy())
-    return dict(s=s, idx=idx, X=X, Q=Q, Qn=Qn, ids=ids.cpu().numpy(), d=d.cpu().numpy(), probes=probes, qr=qr,
+    sub = SubIndex(ex, lists, lambda gids: X[torch.from_numpy(gids - lo).to(dev)].cpu().numpy())
+    return dict(s=s, idx=idx, X=X, Q=Q, Qn=Qn, lo=lo, ids=ids.cpu().numpy(), d=d.cpu().numpy(), probes=probes, qr=qr,
                 topm=dbg["topm_ids"].cpu().numpy(), topm_est=dbg["topm_est"].cpu().numpy(),
                 qscal=dbg["qscal"].cpu().numpy(), sample=sample, ex=ex, sub=sub, nprobe=nprobe)
 
 
 def _check_injected(r, orc):
-    """L5 / L6 per sampled query (qid_base = the query's global row)."""
+    """L1 / L5 / L6 per sampled query (qid_base = the query's global row)."""
     s, sub, nprobe = r["s"], r["sub"], r["nprobe"]
     X = r["X"]
+    # per candidate id: n_o and its list (estimator tolerance of its pair, R#27)
+    gid = sub.global_ids[sub.list_ids]
+    n_o_of = dict(zip(gid.tolist(), sub.n_o.tolist()))
+    lst = np.repeat(np.arange(sub.list_off.size - 1), np.diff(sub.list_off))
+    list_of = dict(zip(gid.tolist(), lst.tolist()))
     ties = 0
     same_final = 0
     for t, q in enumerate(r["sample"]):
+        pu.check_probe_lists(r["probes"][q:q + 1], r["qr"][q:q + 1], r["ex"]["centroids"], nprobe)
         oi, od, _, tids, test = sub.search(orc, r["Qn"][q:q + 1], s.k, nprobe, s.M, s.build_seed,
                                            qr_in=r["qr"][q:q + 1], probes_in=r["probes"][q:q + 1], debug=True,
                                            qid_base=int(q))
@@ -94,21 +107,22 @@ def _check_injected(r, orc):
         a, b = set(gt[gt >= 0].tolist()), set(tids[0][tids[0] >= 0].tolist())
         ties += len(a ^ b)
         if a != b:
-            # every swapped id sits at the M-th boundary within the estimator tolerance (R#18, R#27)
-            nq2 = float(r["qscal"][q, :, 2].max())
-            tol = 4 * pu.est_tol(float(sub.n_o.max()), nq2)
-            g_mth = float(r["topm_est"][q][np.isfinite(r["topm_est"][q])].max())
-            o_mth = float(test[0][np.isfinite(test[0])].max())
-            assert abs(g_mth - o_mth) <= tol, (q, g_mth, o_mth, tol)
+            def tol(x):
+                p = int(np.nonzero(r["probes"][q] == list_of[int(x)])[0][0])
+                return pu.est_tol(float(n_o_of[int(x)]), float(r["qscal"][q, p, 2]))
+
+            fin = np.isfinite(test[0])
+            im = int(np.argmax(np.where(fin, test[0], -np.inf)))
+            o_mth, tol_m = float(test[0][im]), tol(tids[0][im])
             gest = dict(zip(gt.tolist(), r["topm_est"][q].tolist()))
             oest = dict(zip(tids[0].tolist(), test[0].tolist()))
-            for x in a - b:
-                assert gest[x] >= o_mth - tol, (q, x, gest[x], o_mth)
+            for x in a - b:  # the GPU kept x: its estimate ties with the oracle's M-th
+                assert abs(gest[x] - o_mth) <= 2 * tol(x) + tol_m, (q, x, gest[x], o_mth)
             for x in b - a:
-                assert oest[x] >= g_mth - tol, (q, x, oest[x], g_mth)
+                assert abs(oest[x] - o_mth) <= tol(x) + tol_m, (q, x, oest[x], o_mth)
         # L6: oracle exact re-rank of the GPU's top-M
         cand = gt[gt >= 0]
-        rows = X[torch.from_numpy(cand).cuda()].cpu().numpy()
+        rows = X[torch.from_numpy(cand).cuda() - r["lo"]].cpu().numpy()
         ri, rd = orc.rerank(r["Qn"][q:q + 1], rows, np.arange(cand.size, dtype=np.int64)[None], s.k)
         ri = np.where(ri >= 0, cand[np.clip(ri, 0, None)], -1)
         pu.check_final(r["ids"][q:q + 1], r["d"][q:q + 1], ri, rd, s.k)
@@ -117,12 +131,34 @@ def _check_injected(r, orc):
 
 
 def _check_end_to_end(r, orc):
+    """Oracle with its own fp64 rotation and probing; every differing query is
+    explained (module docstring).  Returns (identical fraction, the oracle's
+    final ids, differing result slots)."""
     s, sub, nprobe = r["s"], r["sub"], r["nprobe"]
-    same = 0
+    same, slots, own = 0, 0, []
+    C64 = r["ex"]["centroids"].astype(np.float64)
     for q in r["sample"]:
-        oi, od = sub.search(orc, r["Qn"][q:q + 1], s.k, nprobe, s.M, s.build_seed, qid_base=int(q))
-        same += int(np.array_equal(oi[0], r["ids"][q]))
-    return same / len(r["sample"])
+        oi, od, oprobes, _, _ = sub.search(orc, r["Qn"][q:q + 1], s.k, nprobe, s.M, s.build_seed, qid_base=int(q),
+                                           debug=True)
+        own.append(oi[0])
+        if np.array_equal(oi[0], r["ids"][q]):
+            same += 1
+            continue
+        slots += len(set(oi[0].tolist()) ^ set(r["ids"][q].tolist())) // 2
+        # L1 from scratch: probed sets differ only by near-tied lists (fp64 distances of the
+        # oracle's own q'); the rest is covered by the injected checks (R#30)
+        qd = orc.rotate(r["Qn"][q:q + 1], r["ex"]["rotation"])[0]
+        dd = ((qd[None] - C64) ** 2).sum(1)
+        ga, oa = set(r["probes"][q].tolist()), set(oprobes[0].tolist())
+        if ga != oa:
+            # the GPU's q' (3xTF32, R#30) is within ~1e-5 |q'| of the fp64 one: a distance
+            # moves by <= 2 sqrt(d) e + e^2, e = 1e-4 |q'| (10x margin)
+            kth = float(np.sort(dd)[nprobe - 1])
+            e = 1e-4 * float(np.linalg.norm(qd))
+            for j in ga ^ oa:
+                band = 2 * np.sqrt(max(dd[j], kth)) * e + e * e
+                assert abs(dd[j] - kth) <= 2 * band, (q, j, dd[j], kth, band)
+    return same / len(r["sample"]), np.stack(own), slots
 
 
 def _recall(r):
@@ -134,18 +170,35 @@ def _recall(r):
         dd = torch.zeros(X.shape[0], dtype=torch.float64, device=X.device)
         for r0 in range(0, X.shape[0], 1 << 22):
             dd[r0:r0 + (1 << 22)] = (X[r0:r0 + (1 << 22)] - Q[q]).pow(2).sum(1, dtype=torch.float64)
-        gt.append(torch.topk(dd, s.k, largest=False).indices.cpu().numpy())
+        gt.append(torch.topk(dd, s.k, largest=False).indices.cpu().numpy() + r["lo"])
     gt = np.stack(gt)
-    return pu.recall(r["ids"][r["sample"]], gt, s.k)
+    return pu.recall(r["ids"][r["sample"]], gt, s.k), gt
 
 
 @pytest.mark.parametrize("cfg,nprobe", [(1, None), (2, None), (3, 16), (3, 64), (3, 128), (4, None)])
 def test_fullsize_parity(orc, cfg, nprobe):
     r = _run(cfg, orc, nprobe)
     ties, same_final = _check_injected(r, orc)
-    frac = _check_end_to_end(r, orc)
-    assert frac >= 0.75, frac
-    rec = _recall(r)
-    print(f"CFG{cfg} nprobe={r['nprobe']}: top-M tie swaps {ties}, injected-final identical {same_final}/"
-          f"{len(r['sample'])}, end-to-end identical {frac:.2f}, recall@{r['s'].k} {rec:.3f}")
-    assert rec >= 0.5
+    frac, own, slots = _check_end_to_end(r, orc)
+    rec, gt = _recall(r)
+    rec_o = pu.recall(own, gt, r["s"].k)
+    n = len(r["sample"])
+    print(f"CFG{cfg} nprobe={r['nprobe']}: top-M tie swaps {ties}, injected-final identical {same_final}/{n}, "
+          f"end-to-end identical {frac:.2f} ({slots} differing slots), recall@{r['s'].k} GPU {rec:.3f} "
+          f"oracle {rec_o:.3f}")
+    assert abs(rec - rec_o) <= slots / (n * r["s"].k) + 1e-12, (rec, rec_o, slots)
+
+
+def test_cfg5_shard_proxy_parity(orc):
+    """CFG5 (1e9 x 96) needs 8 GPUs; one GPU holds rank 0's shard exactly as the
+    8-GPU job builds it (bench.py --shard 0/8: ids [0, N/8), P and centroids
+    trained on that slice): the same L1/L5/L6 and end-to-end checks on sampled
+    queries, recall against the shard's own exact kNN."""
+    r = _run(5, orc, shard=(0, 8))
+    ties, same_final = _check_injected(r, orc)
+    frac, own, slots = _check_end_to_end(r, orc)
+    rec, gt = _recall(r)
+    rec_o = pu.recall(own, gt, r["s"].k)
+    print(f"CFG5 shard 0/8: top-M tie swaps {ties}, injected-final identical {same_final}/{len(r['sample'])}, "
+          f"end-to-end identical {frac:.2f}, recall@{r['s'].k} GPU {rec:.3f} oracle {rec_o:.3f}")
+    assert abs(rec - rec_o) <= slots / (len(r["sample"]) * r["s"].k) + 1e-12

@@ -352,12 +352,12 @@ def _pairs(rng, n, D, ip_target=None):
     return o.astype(np.float32), q.astype(np.float32)
 
 
-def _errors(orc, D, n, seed, fourbit):
+def _errors(orc, D, n, seed, fourbit, ip_target=None):
     """<o,q> estimation errors for n random unit pairs (P = I: isotropic pairs
     make the rotation irrelevant), with either the 4-bit query (NS(2)) or the
     exact query residual."""
     rng = np.random.default_rng(seed)
-    o, q = _pairs(rng, n, D)
+    o, q = _pairs(rng, n, D, ip_target)
     codes, n_o, rho = orc.encode(o, np.eye(D, dtype=np.float32), np.zeros((1, D), np.float32),
                                  np.zeros(n, np.int32))
     z = np.zeros(D, np.float32)
@@ -413,6 +413,29 @@ def test_estimator_error_scaling_and_bound(orc):
             assert viol4 <= 0.08
     slope = np.polyfit(np.log(Ds), np.log(sds), 1)[0]
     assert -0.55 <= slope <= -0.45
+
+
+@pytest.mark.parametrize("t", [0.0, 0.5])
+def test_bound_violation_rate_two_sided(orc, t):
+    """Two-sided pin of the error bound (NS(4), eps0 = 1.9, R#14).  At fixed
+    <o,q> = t the exact-query estimator's error is
+        <obar,q>/<obar,o> - t = sqrt(1-rho^2) sqrt(1-t^2) u / rho,
+    u = <e, w> a coordinate of a uniform unit vector in D-1 dimensions,
+    independent of rho (obar = rho o + sqrt(1-rho^2) e, q = t o + sqrt(1-t^2) w,
+    e, w unit and orthogonal to o).  The bound is eps0 sqrt(1-rho^2)/(rho
+    sqrt(D-1)), so P(|err| > bound) = P(|u| > a), a = eps0 / (sqrt(1-t^2)
+    sqrt(D-1)), = I_{1-a^2}((D-2)/2, 1/2) exactly (regularized incomplete beta).
+    The measured rate must lie within 4 SE of it on both sides: a bound 2x too
+    wide (rate ~1e-8) or too narrow (~0.45) fails."""
+    from scipy.special import betainc
+
+    D, n = 128, 20000
+    _, viol = _errors(orc, D, n, 300 + int(10 * t), fourbit=False, ip_target=t)
+    m = D - 1
+    a = 1.9 / (math.sqrt(1 - t * t) * math.sqrt(m))
+    p = float(betainc((m - 1) / 2, 0.5, 1 - a * a))
+    se = math.sqrt(p * (1 - p) / n)
+    assert abs(viol - p) <= 4 * se, (viol, p, se)
 
 
 def test_estimator_special_cases(orc):

@@ -1,6 +1,6 @@
 #!/bin/bash
 # ncu --set full of the small-K scan at CFG4 (main scan launch)
-OUT=gpurun_out/r2c; mkdir -p $OUT
+OUT=gpurun_out/${TAG:-r2c}; mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
 CMD="python bench.py --config 4 --steps 1 --warmup 3 --no-cpu-baseline --no-recall"
 $CMD > $OUT/plain.log 2>&1 && \
