@@ -6,8 +6,9 @@
 A step is one pass of the whole hot path (rotate, probe, quantize, scan +
 estimator, top-M, exact re-rank; + NCCL top-k merge for N > 1) over one batch
 of the config's queries against its index, inputs resident in HBM.  The
-default workload is BASELINE.json configs[1] (CFG2: D=960, N=1e6, nlist=1024,
-10k queries, nprobe=64, k=100, re-rank 1000).  Rank 0 prints ONE JSON line.
+default workload is BASELINE.json configs[3] (CFG4: D=128, N=1e8 uint8-valued
+vectors, nlist=16384, 10k queries, nprobe=64, k=10, re-rank 100), the largest
+configuration that fits one GPU.  Rank 0 prints ONE JSON line.
 
 For N > 1 (torchrun, one process per GPU) the index is sharded by contiguous
 id slices, every rank scans its shard for all queries, and the
@@ -16,8 +17,8 @@ fixed, "scaling": "strong".
 
 --impl reference times the oracle (oracle/, plain C fp64) on this box's host
 cores on the same config/metric, each step a bounded sample of the queries,
-over an index built on the CPU (torch CPU BLAS k-means/assignment + the
-oracle's rotation); rank 0 only.
+over the lists they probe of an index built with plain torch ops (the oracle's
+rotation, torch k-means/assignment; no librabitq kernel); rank 0 only.
 """
 from __future__ import annotations
 
@@ -38,6 +39,7 @@ import torch  # noqa: E402
 import synth  # noqa: E402
 
 METRIC = "QPS at fixed nprobe/k (coarse-scan GB/s vs HBM peak; recall@k vs exact)"
+ALU_OPS_PER_PAIR = 5  # fused estimator + threshold per (query, vector) pair
 
 
 def log(*a):
@@ -199,6 +201,7 @@ def run_ours(args):
     if proxy and world > 1:
         raise SystemExit("--shard is a single-process proxy")
     idx, X, Q = build_shard(s, rank, world, dev, rq, proxy)
+    info = idx.info()
     comm = None
     if world > 1:
         uid = rdist.share_unique_id(rq.Comm.unique_id() if rank == 0 else None)
@@ -208,12 +211,26 @@ def run_ours(args):
     dist = torch.empty(s.nq, s.k, dtype=torch.float32, device=dev)
     flush = torch.zeros(64 << 20, dtype=torch.float32, device=dev)
 
+    # query-split probing in the single-GPU shard proxy: this rank probes its
+    # ceil(nq / G) queries inside the step; the other ranks' lists (which the
+    # all-gather of the real job delivers, 5 MB at CFG5) are precomputed here
+    qs_probes, qs_slice = None, None
+    if proxy and args.query_split:
+        c = (s.nq + proxy[1] - 1) // proxy[1]
+        qs_slice = (proxy[0] * c, min(s.nq, (proxy[0] + 1) * c))
+        qs_probes = idx.probe(Q, s.nprobe, stream=stream)
+        torch.cuda.synchronize()
+
     def step(prof=None):
-        if comm is None:
+        if comm is None and qs_probes is not None:
+            idx.probe(Q[qs_slice[0]:qs_slice[1]], s.nprobe, stream=stream)
+            idx.search(Q, s.k, s.nprobe, s.M, scan_path=args.scan_path, stream=stream, out=(ids, dist),
+                       profile=prof, rerank=args.rerank, query_bits=args.query_bits, probes=qs_probes)
+        elif comm is None:
             idx.search(Q, s.k, s.nprobe, s.M, scan_path=args.scan_path, stream=stream, out=(ids, dist),
                        profile=prof, rerank=args.rerank, query_bits=args.query_bits)
         else:
-            kw = dict(scan_path=args.scan_path, stream=stream.cuda_stream)
+            kw = dict(scan_path=args.scan_path, stream=stream.cuda_stream, query_split=args.query_split)
             if prof is not None:
                 import ctypes
 
@@ -264,7 +281,7 @@ def run_ours(args):
             idx.search(Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path, out=(ih, dh), rerank=args.rerank,
                        query_bits=args.query_bits)
         else:
-            comm.search_sharded(idx, Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path)
+            comm.search_sharded(idx, Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path, query_split=args.query_split)
     barrier()
     et = []
     for _ in range(max(3, min(args.steps, 10))):
@@ -274,7 +291,8 @@ def run_ours(args):
             idx.search(Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path, out=(ih, dh), rerank=args.rerank,
                        query_bits=args.query_bits)
         else:
-            r = comm.search_sharded(idx, Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path)
+            r = comm.search_sharded(idx, Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path,
+                                    query_split=args.query_split)
         et.append(time.perf_counter() - t0)
     log(f"[rank {rank}] e2e ms per call: {[round(t_ * 1e3, 2) for t_ in et]}")
     e2e_t = torch.tensor([sum(et)], dtype=torch.float64, device=dev)
@@ -296,10 +314,20 @@ def run_ours(args):
     rerank_bytes = s.nq * s.M * (4 * s.D + 8) + surv * 8
     int8_peak = 2.0 * pk.get("bf16_tflops", 1590.0)  # dense int8 = 2x bf16 (nominal ratio, B200_PROFILING.md)
     scan_ops = 2.0 * pairs * s.D  # int8 multiply-adds of <b, qbar>, 2 ops each
+    # d <= 128 (the small-K scan): a pair is 4 K-steps of one UMMA but ~5 FP32 lane
+    # operations of the fused estimator + threshold (int->float, 3 FMA, compare;
+    # DESIGN.md sec 6): the FP32 ALU, not the tensor pipe, is the roof
+    alu_peak = 148 * 128 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12  # lane-ops/s, T
+    alu_ops = ALU_OPS_PER_PAIR * pairs
+    scan_tensor = {"bound": "tensor", "achieved": scan_ops / (stage_ms["scan"] * 1e-3) / 1e12, "unit": "TFLOP/s",
+                   "peak": int8_peak, "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (int8:bf16 = 2:1 nominal)",
+                   "algorithmic": scan_ops}
+    scan_alu = {"bound": "alu", "achieved": alu_ops / (stage_ms["scan"] * 1e-3) / 1e12, "unit": "Tops/s",
+                "peak": round(alu_peak, 2), "algorithmic": alu_ops,
+                "peak_source": "148 SMs x 128 FP32 lanes x sm_max_mhz (MEASURED_PEAKS.json), 1 op per lane-instruction"}
+    small_k = imma and s.D <= 128
     rl = {
-        "scan": ({"bound": "tensor", "achieved": scan_ops / (stage_ms["scan"] * 1e-3) / 1e12, "unit": "TFLOP/s",
-                  "peak": int8_peak, "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (int8:bf16 = 2:1 nominal)",
-                  "algorithmic": scan_ops} if imma else
+        "scan": ((scan_alu if small_k else scan_tensor) if imma else
                  {"bound": "hbm", "achieved": scan_bytes / (stage_ms["scan"] * 1e-3) / 1e9, "unit": "GB/s",
                   "peak": pk["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs", "algorithmic": scan_bytes}),
         "select_rerank": {"bound": "hbm", "achieved": rerank_bytes / (stage_ms["select_rerank"] * 1e-3) / 1e9,
@@ -356,6 +384,7 @@ def run_ours(args):
                    "k": s.k, "n_rerank": s.M, "kind": s.kind, "parallelism": (f"shard {args.shard} (single-GPU proxy: one rank's share)" if proxy
                                    else f"list-shards x{world}"),
                    "l2": "flushed between steps (256 MiB write)", "scan_path": args.scan_path,
+                   **({"probing": "query-split" if args.query_split else "replicated"} if (proxy or world > 1) else {}),
                    **({"rerank": "bound-driven (NEXT-4)"} if args.rerank else {}),
                    **({"query": "unquantized, 24-bit fixed point digit rows (NEXT-1)"} if args.query_bits == 32
                       else {})},
@@ -363,6 +392,11 @@ def run_ours(args):
                 "d2h_bytes_per_step": s.nq * s.k * 12 * world},
         "gpu_launches": launches * args.steps,
         "roofline": roofline, "roofline_other": roofline_other, "scan": scan_roof,
+        **({"roofline_tensor": {k_: (round(v, 4) if isinstance(v, float) else v) for k_, v in scan_tensor.items()}
+            | {"frac": round(scan_tensor["achieved"] / scan_tensor["peak"], 4)}} if small_k else {}),
+        "index_bytes": {"total": info["bytes_total"], "codes_and_factors": info["bytes_codes"] + info["bytes_factors"],
+                        "codes8": info["bytes_codes8"], "slot_vectors": info["bytes_slot_vectors"],
+                        "vectors_fp32": s.N * s.D * 4 // max(1, world)},
         "stage_ms": {k_: round(v, 4) for k_, v in stage_ms.items()},
         "survivors_per_query": round(surv / s.nq, 1), "max_survivors": max_surv, "overflow_rescans": retries,
         **({"reranked_per_query": round(float(np.mean([p["reranked"] for p in profs])) / s.nq, 1)}
@@ -385,13 +419,6 @@ def _cores():
         return len(os.sched_getaffinity(0))
     except Exception:
         return os.cpu_count() or 1
-
-
-def _oracle_time(orc, s, ex, Xh, Qh, nqs, threads):  # reference arm (CPU-built index)
-    t0 = time.perf_counter()
-    orc.search(Qh[:nqs], ex["rotation"], ex["centroids"], ex["list_off"], ex["ids"], ex["codes"], ex["n_o"], ex["rho"],
-               Xh, s.k, s.nprobe, s.M, s.build_seed, num_threads=threads)
-    return time.perf_counter() - t0
 
 
 def cpu_baseline(s, idx, X, Q, args, budget_s=20.0):
@@ -427,40 +454,60 @@ def cpu_baseline(s, idx, X, Q, args, budget_s=20.0):
                       f"probed lists, OpenMP {cores} threads, {t:.1f} s"}
 
 
-def reference_index_cpu(s, X, seed):
-    """CPU index for the reference arm: oracle Haar P; k-means (10 Lloyd
-    iterations on 32 nlist rows) and nearest-centroid assignment with torch CPU
-    matmuls; sign codes / factors of the rotated residual; no GPU involved."""
+def reference_index(s, X, seed):
+    """Index for the reference arm, built with plain torch ops (no librabitq
+    kernel; on the GPU when there is one, chunked, so CFG4's 1e8 rows fit): the
+    oracle's Haar P; k-means (10 Lloyd iterations on 32 nlist rows) and
+    nearest-centroid assignment; sign codes and factors of the rotated residual.
+    Returns the export-format dict (list order) the oracle consumes."""
     import oracle as orc
 
+    dev = X.device
     _, P = orc.haar_rotation(s.D, seed)
-    Pt = torch.from_numpy(P)
-    Xr = X @ Pt  # x' = P^T x, row form
+    Pt = torch.from_numpy(P).to(dev)
     g = torch.Generator().manual_seed(seed)
     ts = min(s.N, 32 * s.nlist)
-    T = Xr[torch.randperm(s.N, generator=g)[:ts]]
-    C = T[torch.randperm(ts, generator=g)[: s.nlist]].clone()
+    T = X[torch.randperm(s.N, generator=g)[:ts].to(dev)] @ Pt
+    C = T[torch.randperm(ts, generator=g)[: s.nlist].to(dev)].clone()
+    ch = max(1, (1 << 27) // max(1, s.nlist))  # rows per distance block (~512 MB of fp32)
+
+    def nearest(A):
+        out = torch.empty(A.shape[0], dtype=torch.int64, device=dev)
+        cn = (C * C).sum(1)
+        for r0 in range(0, A.shape[0], ch):
+            blk = A[r0:r0 + ch]
+            out[r0:r0 + ch] = (cn[None, :] - 2.0 * (blk @ C.T)).argmin(1)
+        return out
+
     for _ in range(10):
-        a = torch.cdist(T, C).argmin(1)
+        a = nearest(T)
         Cn = torch.zeros_like(C).index_add_(0, a, T)
-        cnt = torch.bincount(a, minlength=s.nlist).clamp_min(1).unsqueeze(1)
-        C = torch.where(torch.bincount(a, minlength=s.nlist).unsqueeze(1) > 0, Cn / cnt, C)
-    assign = torch.empty(s.N, dtype=torch.int64)
-    for r0 in range(0, s.N, 65536):
-        assign[r0:r0 + 65536] = torch.cdist(Xr[r0:r0 + 65536], C).argmin(1)
+        cnt = torch.bincount(a, minlength=s.nlist)
+        C = torch.where(cnt[:, None] > 0, Cn / cnt.clamp_min(1)[:, None], C)
+    W = s.W
+    assign = torch.empty(s.N, dtype=torch.int64, device=dev)
+    codes = torch.empty(s.N, W, dtype=torch.int64, device=dev)
+    n_o = torch.empty(s.N, dtype=torch.float32, device=dev)
+    rho = torch.empty(s.N, dtype=torch.float32, device=dev)
+    shifts = torch.arange(32, device=dev, dtype=torch.int64)
+    for r0 in range(0, s.N, 1 << 20):
+        Xr = X[r0:r0 + (1 << 20)] @ Pt
+        a = nearest(Xr)
+        R = (Xr - C[a]).double()
+        bits = torch.zeros(R.shape[0], W * 32, dtype=torch.int64, device=dev)
+        bits[:, : s.D] = (R >= 0).long()
+        codes[r0:r0 + R.shape[0]] = (bits.view(-1, W, 32) << shifts).sum(-1)
+        no = R.norm(dim=1)
+        n_o[r0:r0 + R.shape[0]] = no.float()
+        rho[r0:r0 + R.shape[0]] = torch.where(no > 0, R.abs().sum(1) / (np.sqrt(s.D) * no), torch.ones_like(no)).float()
+        assign[r0:r0 + R.shape[0]] = a
     order = torch.argsort(assign, stable=True)
     off = torch.zeros(s.nlist + 1, dtype=torch.int64)
-    off[1:] = torch.cumsum(torch.bincount(assign, minlength=s.nlist), 0)
-    R = (Xr[order] - C[assign[order]]).double()
-    bits = (R >= 0).numpy()
-    W = s.W
-    pad = np.zeros((s.N, W * 32), bool)
-    pad[:, : s.D] = bits
-    codes = np.packbits(pad.reshape(s.N, W, 32), axis=2, bitorder="little").view("<u4").reshape(s.N, W)
-    n_o = R.norm(dim=1)
-    rho = torch.where(n_o > 0, R.abs().sum(1) / (np.sqrt(s.D) * n_o), torch.ones_like(n_o))
-    return dict(rotation=P, centroids=C.numpy(), list_off=off.numpy(), ids=order.numpy().astype(np.int64),
-                codes=codes, n_o=n_o.float().numpy(), rho=rho.float().numpy())
+    off[1:] = torch.cumsum(torch.bincount(assign, minlength=s.nlist).cpu(), 0)
+    return dict(rotation=P.astype(np.float32), centroids=C.float().cpu().numpy(), list_off=off.numpy(),
+                ids=order.cpu().numpy().astype(np.int64),
+                codes=codes[order].cpu().numpy().astype(np.uint32), n_o=n_o[order].cpu().numpy(),
+                rho=rho[order].cpu().numpy())
 
 
 def run_reference(args):
@@ -468,37 +515,52 @@ def run_reference(args):
     if rank != 0:
         return
     import oracle as orc
+    from oracle.subindex import SubIndex
 
     orc.build()
     s = workload(args)
     t0 = time.time()
-    cen = synth.centres(s, "cpu")
-    X = synth.base_rows(s, 0, s.N, "cpu", cen=cen)
-    Q = synth.queries(s, "cpu", cen=cen)
-    ex = reference_index_cpu(s, X, s.build_seed)
-    log(f"[reference] data + CPU index {time.time() - t0:.1f}s")
-    Xh, Qh = X.numpy(), Q.numpy()
+    dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
+    cen = synth.centres(s, dev)
+    X = synth.base_rows(s, 0, s.N, dev, cen=cen)
+    Q = synth.queries(s, dev, cen=cen)
+    ex = reference_index(s, X, s.build_seed)
+    Qh = Q.cpu().numpy()
+    log(f"[reference] data + index (torch ops on {dev.type}) {time.time() - t0:.1f}s")
     cores = _cores()
+
+    def sub_for(qs):  # the oracle's own probes of these queries -> the lists it will read
+        lists = np.unique(np.concatenate([orc.probe(orc.rotate(Qh[q:q + 1], ex["rotation"])[0].astype(np.float32),
+                                                    ex["centroids"], s.nprobe) for q in qs]))
+        return SubIndex(ex, lists, lambda gids: X[torch.from_numpy(gids).to(dev)].cpu().numpy())
+
+    def timed(sub, q0, n):
+        t = time.perf_counter()
+        sub.search(orc, Qh[q0:q0 + n], s.k, s.nprobe, s.M, s.build_seed, qid_base=q0, num_threads=cores)
+        return time.perf_counter() - t
+
     n0 = min(s.nq, max(2, cores))
-    t = _oracle_time(orc, s, ex, Xh, Qh, n0, cores)
+    t = timed(sub_for(range(n0)), 0, n0)
     per_step_budget = max(2.0, 150.0 / max(1, args.steps + args.warmup))
     nqs = int(min(s.nq, max(1, n0 * per_step_budget / max(t, 1e-3))))
+    pool = min(s.nq, nqs * (args.steps + args.warmup))
+    sub = sub_for(range(pool))
+    starts = [(i * nqs) % max(1, pool - nqs + 1) for i in range(args.steps + args.warmup)]
     for w in range(args.warmup):
-        _oracle_time(orc, s, ex, Xh, Qh[w * nqs % max(1, s.nq - nqs):], nqs, cores)
-    tt = []
-    for i in range(args.steps):
-        q0 = (i * nqs) % max(1, s.nq - nqs + 1)
-        tt.append(_oracle_time(orc, s, ex, Xh, Qh[q0:], nqs, cores))
+        timed(sub, starts[w], nqs)
+    tt = [timed(sub, starts[args.warmup + i], nqs) for i in range(args.steps)]
     qps = nqs * len(tt) / sum(tt)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(qps, 3), "unit": "queries/s", "n_gpus": int(
             os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * sum(tt) / len(tt), 3), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64 (oracle)", "data": "synthetic (synth/, CPU)",
+        "vs_baseline": None, "dtype": "f64 (oracle)", "data": "synthetic (synth/, same generator as the GPU arm)",
         "config": {"workload": f"CFG{s.cfg}", "D": s.D, "N": s.N, "nlist": s.nlist, "nq": s.nq, "nprobe": s.nprobe,
                    "k": s.k, "n_rerank": s.M, "queries_per_step": nqs},
         "cpu_baseline": {"value": round(qps, 3), "unit": "queries/s", "cores": cores, "kind": "oracle",
-                         "sample": f"{nqs} queries per step of CFG{s.cfg}, oracle over a CPU-built index"},
+                         "sample": f"{nqs} queries per step of CFG{s.cfg}, the full oracle path (fp64 rotate/probe, "
+                                   f"pinned fp32 quantizer, plain-loop ip, fp64 estimator, full sort, fp64 re-rank) "
+                                   f"over the lists they probe of an index built with torch ops (no librabitq)"},
         "e2e": {"value": round(qps, 3), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -554,7 +616,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4,
+                    help="BASELINE.json configs[C-1]; default 4 = the largest single-GPU config (N = 1e8)")
     ap.add_argument("--nq", type=int, default=0, help="override the query count (quick runs)")
     ap.add_argument("--nprobe", type=int, default=0, help="override nprobe (CFG3's sweep: 16/32/64/128)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
@@ -567,6 +630,8 @@ def main():
                     help="1: bound-driven re-rank set (NEXT-4; changes results, opt-in)")
     ap.add_argument("--workload", choices=["search", "build"], default="search",
                     help="build: time rabitq_build (NEXT-3) instead of the search hot path")
+    ap.add_argument("--query-split", type=int, default=1, choices=[0, 1], dest="query_split",
+                    help="N > 1 / --shard: 1 = each rank probes nq/G queries, probe lists all-gathered (SURVEY 8(e))")
     ap.add_argument("--shard", default="", help="r/G: time shard r of G on one GPU (per-GPU proxy for configs "
                     "that need G GPUs, e.g. CFG5); the line then reports that shard's QPS")
     args = ap.parse_args()

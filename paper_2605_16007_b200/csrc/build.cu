@@ -22,6 +22,7 @@
 
 #include "index.cuh"
 #include "search.cuh"
+#include "tgemm.cuh"
 
 namespace rabitq {
 namespace {
@@ -135,6 +136,23 @@ __global__ void argmin_kernel(const float* __restrict__ dist, int64_t m, int nli
         if (bi == 0x7FFFFFFF) bi = 0;  // all-NaN row cannot happen (inputs checked finite)
         assign[row] = bi;
         if (best) best[row] = bv;
+        if (prev) {
+            if (prev[row] != bi) atomicAdd(changed, 1ull);
+            prev[row] = bi;
+        }
+    }
+}
+
+// the same outputs from the tensor-core GEMM's fused argmin (tgemm TG_EPI_ARGMIN):
+// key = orderable(||c||^2 - 2 x.c) << 32 | centroid
+__global__ void argmin_keys_kernel(const unsigned long long* __restrict__ keys, int64_t m,
+                                   int32_t* __restrict__ assign, float* __restrict__ best,
+                                   int32_t* __restrict__ prev, unsigned long long* __restrict__ changed) {
+    for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < m; row += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long k = keys[row];
+        const int bi = (int)(uint32_t)k;
+        assign[row] = bi;
+        if (best) best[row] = o2f((uint32_t)(k >> 32));
         if (prev) {
             if (prev[row] != bi) atomicAdd(changed, 1ull);
             prev[row] = bi;
@@ -379,7 +397,34 @@ void build_index(rabitq_index* idx, const float* X, int64_t n, int D, int nlist,
     // distance block budget: rows per chunk so that [rows x nlist] fp32 <= ~1 GiB
     const int64_t chunk_rows = std::max<int64_t>(
         1024, std::min<int64_t>(std::min<int64_t>(n, 1 << 20), ((int64_t)1 << 28) / std::max(nlist, 1)));
-    DBuf<float> dist((size_t)chunk_rows * nlist);
+    // distance GEMM + argmin: 3xTF32 tensor cores with the argmin fused into the
+    // epilogue (no distance matrix; NEXT-3) when D % 4 == 0, else fp32 SIMT
+    const bool tc_dist = D % 4 == 0 && !rq_diag_env("RABITQ_SIMT_GEMM");
+    DBuf<float> dist(tc_dist ? 0 : (size_t)chunk_rows * nlist);
+    DBuf<unsigned long long> akeys(tc_dist ? (size_t)chunk_rows : 0);
+    auto nearest = [&](const float* A, int64_t m, int32_t* a_out, float* best, int32_t* prev,
+                       unsigned long long* changed) {
+        if (tc_dist) {
+            RQ_CUDA(cudaMemsetAsync(akeys.p, 0xFF, (size_t)m * sizeof(unsigned long long), st));
+            TgParams g{};
+            g.A = A;
+            g.lda = D;
+            g.B = idx->Cr;
+            g.ldb = D;
+            g.K = D;
+            g.M = m;
+            g.N = nlist;
+            g.b_norm = idx->cnorm;
+            g.amin = akeys.p;
+            tgemm(g, TG_EPI_ARGMIN, st);
+            argmin_keys_kernel<<<grid_for(m), 256, 0, st>>>(akeys.p, m, a_out, best, prev, changed);
+            RQ_CHECK_LAUNCH();
+        } else {
+            sgemm((int)m, nlist, D, A, D, idx->Cr, D, true, dist.p, nlist, 1, idx->cnorm, st);
+            argmin_kernel<<<(int)((m * 32 + 255) / 256), 256, 0, st>>>(dist.p, m, nlist, a_out, best, prev, changed);
+            RQ_CHECK_LAUNCH();
+        }
+    };
 
     // ---- k-means in the rotated space ----
     if (o.centroids_rot) {
@@ -424,10 +469,7 @@ void build_index(rabitq_index* idx, const float* X, int64_t n, int D, int nlist,
             RQ_CUDA(cudaMemsetAsync(changed.p, 0, sizeof(unsigned long long), st));
             for (int64_t r0 = 0; r0 < ts; r0 += chunk_rows) {
                 const int64_t m = std::min(chunk_rows, ts - r0);
-                sgemm((int)m, nlist, D, Tr.p + (size_t)r0 * D, D, idx->Cr, D, true, dist.p, nlist, 1, idx->cnorm, st);
-                argmin_kernel<<<(int)((m * 32 + 255) / 256), 256, 0, st>>>(dist.p, m, nlist, ta.p + r0, tbest.p + r0,
-                                                                             tprev.p + r0, changed.p);
-                RQ_CHECK_LAUNCH();
+                nearest(Tr.p + (size_t)r0 * D, m, ta.p + r0, tbest.p + r0, tprev.p + r0, changed.p);
             }
             unsigned long long hchanged = 0;
             RQ_CUDA(cudaMemcpyAsync(&hchanged, changed.p, sizeof(hchanged), cudaMemcpyDeviceToHost, st));
@@ -476,10 +518,7 @@ void build_index(rabitq_index* idx, const float* X, int64_t n, int D, int nlist,
         for (int64_t r0 = 0; r0 < n; r0 += chunk_rows) {
             const int64_t m = std::min(chunk_rows, n - r0);
             sgemm((int)m, D, D, Xd + (size_t)r0 * D, D, idx->P, D, false, xr.p, D, 0, nullptr, st);
-            sgemm((int)m, nlist, D, xr.p, D, idx->Cr, D, true, dist.p, nlist, 1, idx->cnorm, st);
-            argmin_kernel<<<(int)((m * 32 + 255) / 256), 256, 0, st>>>(dist.p, m, nlist, assign.p + r0, nullptr,
-                                                                         nullptr, nullptr);
-            RQ_CHECK_LAUNCH();
+            nearest(xr.p, m, assign.p + r0, nullptr, nullptr, nullptr);
             encode_kernel<<<(int)((m * 32 + 255) / 256), 256, 0, st>>>(xr.p, m, D, W, idx->Cr, assign.p + r0,
                                                                          codes_id.p + (size_t)r0 * W, no_id.p + r0,
                                                                          rho_id.p + r0);
@@ -487,6 +526,7 @@ void build_index(rabitq_index* idx, const float* X, int64_t n, int D, int nlist,
         }
     }
     dist.release();
+    akeys.release();
 
     // ---- lists: sizes, offsets, 32-aligned slots ----
     DBuf<int64_t> hist(nlist);

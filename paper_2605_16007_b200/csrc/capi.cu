@@ -243,7 +243,7 @@ rabitq_status rabitq_search(const rabitq_index* idx, const float* Q, int64_t nq,
 
 static void search_local(const rabitq_index* idx, const float* Q, int64_t nq, int k, int nprobe, int M,
                          const rabitq_search_opts& o, int64_t* ids_d, float* dists_d, cudaStream_t st,
-                         const float* Qd) {
+                         const float* Qd, bool trusted_probes = false) {
     (void)Q;
     rabitq::SearchCfg cfg;
     cfg.scan_path = o.scan_path;
@@ -302,6 +302,7 @@ static void search_local(const rabitq_index* idx, const float* Q, int64_t nq, in
         RQ_CUDA(cudaMemcpyAsync(sp.p, o.probes_in, (size_t)nq * nprobe * sizeof(int32_t), cudaMemcpyHostToDevice, st));
         probes_d = (const int32_t*)sp.p;
     }
+    if (probes_d && !trusted_probes) rabitq::check_probes(probes_d, (int64_t)nq * nprobe, idx->nlist, st);
     rabitq::SearchStats stats;
     stats.timing = o.profile != nullptr;
     for (int64_t b0 = 0; b0 < nq; b0 += qbatch) {
@@ -562,7 +563,8 @@ rabitq_status rabitq_search_sharded(const rabitq_index* shard, rabitq_comm* comm
         RQ_REQUIRE(r == ncclSuccess, RABITQ_ERR_NCCL, std::string("ncclAllGather (probes): ") + ncclGetErrorString(r));
         o.probes_in = (const int32_t*)pg.p;
     }
-    search_local(shard, Q, nq, k, nprobe, n_rerank, o, (int64_t*)li.p, (float*)ld.p, st, Qd);
+    search_local(shard, Q, nq, k, nprobe, n_rerank, o, (int64_t*)li.p, (float*)ld.p, st, Qd,
+                 /*trusted_probes=*/o.query_split && G > 1 && !(opts && opts->probes_in));
     // the one exchange step: all-gather of the per-rank top-k over NVLink
     ncclResult_t r = ncclGroupStart();
     if (r == ncclSuccess) r = ncclAllGather(li.p, gi.p, nk, ncclInt64, comm->comm, st);

@@ -1,6 +1,8 @@
 // search.cuh -- argument blocks shared by the scan kernels (popc: search.cu,
 // tcgen05 IMMA: scan_imma.cu) and the host orchestration.
 #pragma once
+#include <nvtx3/nvToolsExt.h>
+
 #include "index.cuh"
 
 namespace rabitq {
@@ -187,15 +189,27 @@ struct SearchStats {
 };
 
 // per-stage CUDA events on the call's stream (rabitq_profile)
+// and NVTX ranges named after the stages (host-side ranges around each stage's
+// enqueue; visible to nsys / ncu --nvtx)
 struct StageTimer {
     cudaEvent_t ev[9] = {};
     bool on = false;
+    int open = -1;  // NVTX range currently pushed
     cudaStream_t st = nullptr;
     StageTimer(bool enable, cudaStream_t s) : on(enable), st(s) {
         if (on)
             for (auto& e : ev) RQ_CUDA(cudaEventCreate(&e));
     }
     void mark(int i) {
+        static const char* kNames[8] = {"rabitq:S1 rotate",      "rabitq:S2-S3 probe",  "rabitq:S4 quantize",
+                                        "rabitq:S5 plan",        "rabitq:S8a seed",     "rabitq:S6-S7 scan",
+                                        "rabitq:overflow rescan", "rabitq:S8b-S9 select+rerank"};
+        if (open >= 0) nvtxRangePop();
+        open = -1;
+        if (i < 8) {
+            nvtxRangePushA(kNames[i]);
+            open = i;
+        }
         if (on) RQ_CUDA(cudaEventRecord(ev[i], st));
     }
     void accumulate(float* ms) {
@@ -208,6 +222,7 @@ struct StageTimer {
         }
     }
     ~StageTimer() {
+        if (open >= 0) nvtxRangePop();
         if (on)
             for (auto& e : ev) cudaEventDestroy(e);
     }
@@ -223,6 +238,7 @@ void group_items(const rabitq_index* idx, const int64_t* list_off, const Groups&
                  WBuf<int64_t>& items, cudaStream_t st, int& launches);
 uint64_t selftest_div(uint64_t n, uint64_t seed, cudaStream_t st);
 void scan_popc_entry(const ScanArgs& a, bool lb, bool retry, bool dump, cudaStream_t st);
+void check_probes(const int32_t* probes, int64_t n, int nlist, cudaStream_t st);
 void probe_only(const rabitq_index* idx, const float* Q, int64_t nq, int nprobe, uint32_t variant, int32_t* probes,
                 cudaStream_t st);
 void merge_topk(const int64_t* in_ids, const float* in_d, int G, int64_t nq, int k, int64_t* out_ids,

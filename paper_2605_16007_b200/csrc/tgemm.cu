@@ -322,7 +322,7 @@ __global__ __launch_bounds__(kNT, 1) void tgemm_kernel(const __grid_constant__ C
             tc::mbar_wait(&normf_bar[b], ub & 1);
             float an = 0.0f;
             if constexpr (kEpi == TG_EPI_DIST) an = __fadd_rn(anorm[(b * 2) * kBM + r], anorm[(b * 2 + 1) * kBM + r]);
-            if constexpr (kEpi != TG_EPI_DIST) {
+            if constexpr (kEpi != TG_EPI_DIST && kEpi != TG_EPI_ARGMIN) {
                 // row-major C: 32 x 32 blocks transposed through shared memory so
                 // that each store instruction writes 32 consecutive columns of a row
                 float* stg = stage + (warp - kEpiWarp0) * kStg;
@@ -347,6 +347,29 @@ __global__ __launch_bounds__(kNT, 1) void tgemm_kernel(const __grid_constant__ C
                     }
                     __syncwarp();
                 }
+                tc::fence_before_sync();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&acce_bar[b]);
+                continue;
+            }
+            if constexpr (kEpi == TG_EPI_ARGMIN) {
+                // nearest B row of this A row within the tile: (orderable key << 32 | id)
+                unsigned long long best = ~0ull;
+                for (int c0 = 0; c0 < ti.n; c0 += 16) {
+                    uint32_t acc[16];
+                    tc::tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * kBN + c0), acc);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int col = c0 + i;
+                        if (col < ti.n) {
+                            const float d = __fmaf_rn(-2.0f, __uint_as_float(acc[i]), __ldg(p.b_norm + ti.b0 + col));
+                            const unsigned long long key =
+                                ((unsigned long long)f2o(d) << 32) | (unsigned long long)(ti.b0 + col);
+                            best = key < best ? key : best;
+                        }
+                    }
+                }
+                if (rok) atomicMin(p.amin + ti.a0 + r, best);
                 tc::fence_before_sync();
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&acce_bar[b]);
@@ -577,6 +600,10 @@ void tgemm(const TgParams& p, int epi, cudaStream_t st) {
     } else if (epi == TG_EPI_PROBE) {
         if (tma) RQ_TG(TG_EPI_PROBE, true);
         else RQ_TG(TG_EPI_PROBE, false);
+    } else if (epi == TG_EPI_ARGMIN) {
+        RQ_REQUIRE(p.tiles == nullptr && p.amin != nullptr, RABITQ_ERR_INTERNAL, "tgemm argmin: plain mode");
+        if (tma) RQ_TG(TG_EPI_ARGMIN, true);
+        else RQ_TG(TG_EPI_ARGMIN, false);
     } else {
         if (tma) RQ_TG(TG_EPI_DIST, true);
         else RQ_TG(TG_EPI_DIST, false);

@@ -475,6 +475,19 @@ def test_edge_cases():
     with pytest.raises(rq.RabitqError) as e:
         idx.search(bad.cuda(), 5, 3, 10)
     assert e.value.status == rq.ERR_INVALID_DATA
+    # >= 256 queries: the side-stream dense re-rank block is in flight when the
+    # error is raised; the workspace it reads must outlive it (no corruption of
+    # the next searches)
+    _, Qbig = make_data(32, 500, 50, 400)
+    ref_i, ref_d = idx.search(Qbig.cuda(), 5, 3, 10)
+    badbig = Qbig.clone()
+    badbig[300, 1] = float("inf")
+    for _ in range(3):
+        with pytest.raises(rq.RabitqError) as e:
+            idx.search(badbig.cuda(), 5, 3, 10)
+        assert e.value.status == rq.ERR_INVALID_DATA
+        again_i, again_d = idx.search(Qbig.cuda(), 5, 3, 10)
+        assert torch.equal(again_i, ref_i) and torch.equal(again_d, ref_d)
     Xb = X.clone()
     Xb[0, 0] = float("inf")
     with pytest.raises(rq.RabitqError) as e:
@@ -498,7 +511,10 @@ def test_degenerate_inputs(orc, scan_path):
     Q = Q.clone()
     Q[0] = X[100]                       # on the singleton centroid
     Q[1] = X[50] + 0.01                 # next to the duplicates
-    idx = build(X, 17)
+    # k-means seeded with the outlier as its own centroid, every row in training:
+    # its cluster stays a singleton (centroid = the point itself)
+    C0 = torch.cat([X[torch.arange(16) * 300 + 7], X[100:101]])
+    idx = build(X, 17, init_centroids=C0, train_size=6000)
     ex = idx.export()
     r = int(np.nonzero(ex["ids"] == 100)[0][0])
     assert ex["n_o"][r] == 0.0 and ex["rho"][r] == 1.0
