@@ -1,4 +1,4 @@
-"""Host-side pieces of bench.py (CPU): the reference arm's CPU index matches
+"""Host-side pieces of bench.py (CPU): the reference arm's torch-built index (run here on the CPU) matches
 the oracle's encode of the same P / centroids / assignment."""
 import numpy as np
 import torch
@@ -7,11 +7,11 @@ import bench
 import synth
 
 
-def test_reference_index_cpu_encode_matches_oracle(orc):
+def test_reference_index_encode_matches_oracle(orc):
     s = synth.spec(1, D=40, N=3000, ncent=12, nlist=12, nq=5)
     cen = synth.centres(s, "cpu")
     X = synth.base_rows(s, 0, s.N, "cpu", cen=cen)
-    ex = bench.reference_index_cpu(s, X, 3)
+    ex = bench.reference_index(s, X, 3)
     off, ids = ex["list_off"], ex["ids"]
     assign = np.empty(s.N, np.int32)
     for j in range(s.nlist):
