@@ -89,6 +89,12 @@ void require_sm100(int dev) {
     }
 }
 
+// one NVTX push/pop range per public call (profilers filter on "rabitq:search" etc.)
+struct NvtxScope {
+    explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+    ~NvtxScope() { nvtxRangePop(); }
+};
+
 // device staging buffer (stream ordered)
 struct Stage {
     void* p = nullptr;
@@ -380,6 +386,7 @@ static void check_search_args(const rabitq_index* idx, const float* Q, int64_t n
 rabitq_status rabitq_search_ex(const rabitq_index* idx, const float* Q, int64_t nq, int32_t k, int32_t nprobe,
                                int32_t n_rerank, const rabitq_search_opts* opts, int64_t* ids, float* dists) {
     API_BEGIN
+    NvtxScope nvtx_scope("rabitq:search");
     check_search_args(idx, Q, nq, k, nprobe, n_rerank, ids, dists);
     if (nq == 0) return RABITQ_OK;
     rabitq_search_opts o;
@@ -464,6 +471,7 @@ rabitq_status rabitq_index_export(const rabitq_index* idx, rabitq_export_t* out)
 rabitq_status rabitq_probe(const rabitq_index* idx, const float* Q, int64_t nq, int32_t nprobe, int32_t* probes,
                            void* stream) {
     API_BEGIN
+    NvtxScope nvtx_scope("rabitq:probe");
     RQ_REQUIRE(idx != nullptr, RABITQ_ERR_INVALID_ARGUMENT, "index is NULL");
     RQ_REQUIRE(nq >= 0 && nprobe >= 0, RABITQ_ERR_INVALID_ARGUMENT, "nq < 0 or nprobe < 0");
     if (nprobe == 0) nprobe = std::max(1, (int)std::ceil(0.05 * idx->nlist));  // AUTO
@@ -531,6 +539,7 @@ rabitq_status rabitq_search_sharded(const rabitq_index* shard, rabitq_comm* comm
                                     int32_t k, int32_t nprobe, int32_t n_rerank, const rabitq_search_opts* opts,
                                     int64_t* ids, float* dists) {
     API_BEGIN
+    NvtxScope nvtx_scope("rabitq:search_sharded");
     check_search_args(shard, Q, nq, k, nprobe, n_rerank, ids, dists);
     RQ_REQUIRE(comm != nullptr, RABITQ_ERR_INVALID_ARGUMENT, "comm is NULL");
     RQ_REQUIRE(comm->device == shard->device, RABITQ_ERR_INVALID_ARGUMENT, "comm and shard on different devices");

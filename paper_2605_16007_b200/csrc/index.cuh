@@ -28,6 +28,7 @@ struct rabitq_index {
     int64_t* list_off = nullptr;   // [nlist + 1] list boundaries in list order (rank of vector)
     int64_t* slot_off = nullptr;   // [nlist + 1] 32-aligned slot starts
     uint32_t* codes = nullptr;     // [nslots / 32][W][32]
+    bool codes8_f8 = false;        // codes8 bytes are e4m3 {0, -1.0} (D <= 128) rather than s8 {0, -1}
     uint8_t* codes8 = nullptr;     // [nslots + 128][32 W] the codes as s8 {0, -1} in the grouped scan's K
                                    // order (scan_imma.cu expand32), slot-major: its A operand by TMA;
                                    // nullable (built when it fits)

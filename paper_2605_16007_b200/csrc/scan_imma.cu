@@ -170,11 +170,25 @@ __device__ __forceinline__ void expand32(uint32_t x, uint4& lo, uint4& hi) {
     hi.w = sgnrep(x * 128u);
 }
 
+// the same bytes as e4m3: -1.0 (0xB8) / 0 (the .kind::f8f6f4 A operand, D <= 128)
+__device__ __forceinline__ void to_e4m3(uint4& lo, uint4& hi) {
+    lo.x &= 0xB8B8B8B8u; lo.y &= 0xB8B8B8B8u; lo.z &= 0xB8B8B8B8u; lo.w &= 0xB8B8B8B8u;
+    hi.x &= 0xB8B8B8B8u; hi.y &= 0xB8B8B8B8u; hi.z &= 0xB8B8B8B8u; hi.w &= 0xB8B8B8B8u;
+}
+
 // fused estimator from the accumulator (acc = -ip: s8 codes in {0, -1}).
 // 0x4B400000 + n is the float 1.5 2^23 + n exactly for |n| < 2^22, so ipn = -ip
 // exactly; the rest is rabitq_est's arithmetic (a ip = (-a)(-ip) exactly).
+// kF8 (e4m3 operands, f32 accumulator, D <= 128): the accumulator is -ip as an
+// exact float already (integers of magnitude <= 15 D < 2^11)
+template <bool kF8 = false>
+__device__ __forceinline__ float acc_ipn(uint32_t acc) {
+    if constexpr (kF8) return __uint_as_float(acc);
+    else return __fsub_rn(__int_as_float(0x4B400000 + (int)acc), 12582912.0f);
+}
+template <bool kF8 = false>
 __device__ __forceinline__ float est_of(uint32_t acc, const ColC& cc, float2 fac, float pcf) {
-    const float ipn = __fsub_rn(__int_as_float(0x4B400000 + (int)acc), 12582912.0f);
+    const float ipn = acc_ipn<kF8>(acc);
     const float tt = __fmaf_rn(-cc.a, ipn, __fmaf_rn(cc.b, pcf, -cc.K));
     return __fmaf_rn(-fac.y, tt, __fadd_rn(fac.x, cc.nq2));
 }
@@ -264,7 +278,7 @@ __device__ __forceinline__ void pos_next(const ScanArgs& a, int NG, int nchunks,
 //              item), chunk c of the next item as soon as chunk c is free
 //   warps 6-13 epilogue: tcgen05.ld the int32 inner products, fused
 //              estimator (+ bound), threshold, survivor append
-template <bool kLB, bool kDump, bool kRetry, bool kDense, bool kTA, bool kFull>
+template <bool kLB, bool kDump, bool kRetry, bool kDense, bool kTA, bool kFull, bool kF8>
 __global__ __launch_bounds__(n_threads(kTA), 1) void scan_imma_kernel(const __grid_constant__ CUtensorMap tmapB,
                                                                       const __grid_constant__ CUtensorMap tmapA,
                                                                       ScanArgs a) {
@@ -348,12 +362,16 @@ __global__ __launch_bounds__(n_threads(kTA), 1) void scan_imma_kernel(const __gr
             const uint32_t dst = tmemA + (uint32_t)(s * kChunkCols) + lane_addr;
             uint4 lo, hi;
             expand32(wv.x, lo, hi);
+            if (kF8) to_e4m3(lo, hi);
             tc::tmem_st8(dst, lo, hi);
             expand32(wv.y, lo, hi);
+            if (kF8) to_e4m3(lo, hi);
             tc::tmem_st8(dst + 8, lo, hi);
             expand32(wv.z, lo, hi);
+            if (kF8) to_e4m3(lo, hi);
             tc::tmem_st8(dst + 16, lo, hi);
             expand32(wv.w, lo, hi);
+            if (kF8) to_e4m3(lo, hi);
             tc::tmem_st8(dst + 24, lo, hi);
             tc::tmem_st_wait();
             tc::fence_before_sync();
@@ -378,7 +396,7 @@ __global__ __launch_bounds__(n_threads(kTA), 1) void scan_imma_kernel(const __gr
         const uint64_t bdesc0 = tc::smem_desc_sw128(tc::smem_u32(Bres));
         for (int64_t item = blockIdx.x; item < total; item += gridDim.x, ++ic) {
             const Item it = decode_item(a, NG, item);
-            const uint32_t idesc = tc::idesc_i8(kTM, it.ncols16, /*a_signed=*/true);
+            const uint32_t idesc = tc::idesc_scan<kF8>(kTM, it.ncols16);
             for (int t = 0; t < it.ntiles; ++t, ++tcnt) {
                 const int b = tcnt & 1;
                 const uint32_t ub = tcnt >> 1;
@@ -399,11 +417,11 @@ __global__ __launch_bounds__(n_threads(kTA), 1) void scan_imma_kernel(const __gr
                         if constexpr (kTA) {
                             // A stage s (TMA, 128-byte swizzle) free once these retire
                             const uint64_t ad = tc::smem_desc_sw128(tc::smem_u32(smem + sp.off_raw + s * kAStage));
-                            tc::mma_i8_ss_chunk(dacc, ad, bd, idesc, c > 0 ? 1u : 0u, nks, &empty_bar[s]);
+                            tc::mma_i8_ss_chunk<kF8>(dacc, ad, bd, idesc, c > 0 ? 1u : 0u, nks, &empty_bar[s]);
                         } else {
                             // nks UMMAs + commit: A slot s free once these retire
                             const uint32_t aaddr = tmemA + (uint32_t)(s * kChunkCols);
-                            tc::mma_i8_ts_chunk(dacc, aaddr, bd, idesc, c > 0 ? 1u : 0u, nks, &empty_bar[s]);
+                            tc::mma_i8_ts_chunk<kF8>(dacc, aaddr, bd, idesc, c > 0 ? 1u : 0u, nks, &empty_bar[s]);
                         }
                         if (t == it.ntiles - 1) tc::commit_warp(&bfree_bar[c]);  // B chunk c free for the next item
                         if (c == nchunks - 1) tc::commit_warp(&accf_bar[b]);     // accumulator b complete
@@ -521,7 +539,7 @@ __global__ __launch_bounds__(n_threads(kTA), 1) void scan_imma_kernel(const __gr
                     constexpr int kStep = kFull ? 4 : 1;
                     auto est_at = [&](int i, const ColC& cc) -> float {
                         if constexpr (kFull) return est_ipn(ipn_full(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]), cc, fac, pcf);
-                        else return est_of(acc[i], cc, fac, pcf);
+                        else return est_of<kF8>(acc[i], cc, fac, pcf);
                     };
                     if constexpr (kDense) {
                         // sample scan: every key, coalesced (lanes = consecutive vectors);
@@ -550,8 +568,9 @@ __global__ __launch_bounds__(n_threads(kTA), 1) void scan_imma_kernel(const __gr
                         for (int i = 0; i < kEC; i += 2) {
                             const float4* P = P0 + 2 * i;  // record (col0 + i) / 2 = 4 float4
                             const float4 ab = P[0], ku = P[1];  // (-a0, -a1, b0, b1), (-K0, -K1, U0, U1)
-                            const float2 ipn = fsub2(make_float2(__int_as_float(0x4B400000 + (int)acc[i]),
-                                                                 __int_as_float(0x4B400000 + (int)acc[i + 1])), mg2);
+                            const float2 ipn = kF8 ? make_float2(__uint_as_float(acc[i]), __uint_as_float(acc[i + 1]))
+                                                   : fsub2(make_float2(__int_as_float(0x4B400000 + (int)acc[i]),
+                                                                       __int_as_float(0x4B400000 + (int)acc[i + 1])), mg2);
                             const float2 inner = ffma2(make_float2(ab.z, ab.w), pc2, make_float2(ku.x, ku.y));
                             const float2 tt = ffma2(make_float2(ab.x, ab.y), ipn, inner);
                             const float2 v = ffma2(nf2, tt, fx2);
@@ -570,7 +589,7 @@ __global__ __launch_bounds__(n_threads(kTA), 1) void scan_imma_kernel(const __gr
                                 if (vok && col0 + i < it.ncols) {
                                     const int64_t di = (a.item_off[cc.pair] + (v >> 5)) * 32 + (v & 31);
                                     if (di < a.dump_cap) {
-                                        a.dump_ip[di] = kFull ? 0 : -(int)acc[i];  // (full: ip exceeds int32)
+                                        a.dump_ip[di] = kFull ? 0 : (int)-acc_ipn<kF8>(acc[i]);  // (full: ip exceeds int32)
                                         a.dump_est[di] = est;
                                     }
                                 }
@@ -626,7 +645,7 @@ __global__ __launch_bounds__(n_threads(kTA), 1) void scan_imma_kernel(const __gr
                             if ((bal >> lane) & 1u) {
                                 const ColC cc = colp_get(cb, col0 + i);
                                 const float est = kFull ? est_ipn(ipn_full(acci, acc1, acc2, acc3), cc, fac, pcf)
-                                                        : est_of(acci, cc, fac, pcf);
+                                                        : est_of<kF8>(acci, cc, fac, pcf);
                                 const float key = rank_key<kLB>(est, epsnq_of(cc), g1);
                                 const int pos = base + __popc(bal & ((1u << lane) - 1u));
                                 if (pos < a.cap) a.buf[(size_t)cc.q * a.cap + pos] = make_key(key, row);
@@ -764,13 +783,14 @@ __global__ void list_items_kernel(int nlist, const int64_t* __restrict__ list_of
 // codes -> s8 {0, -1} rows in the K order of expand32 (the TMEM A operand the
 // producers would build), slot-major, 128 zero pad rows
 __global__ void expand_codes_kernel(const uint32_t* __restrict__ codes, int64_t nslots, int W,
-                                    uint4* __restrict__ out) {
+                                    uint4* __restrict__ out, bool f8) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (nslots + kTM) * W;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t s = e / W;
         const int w = (int)(e % W);
         uint4 lo = make_uint4(0u, 0u, 0u, 0u), hi = lo;
         if (s < nslots) expand32(__ldg(codes + ((s >> 5) * W + w) * 32 + (s & 31)), lo, hi);
+        if (f8) to_e4m3(lo, hi);
         out[2 * e] = lo;
         out[2 * e + 1] = hi;
     }
@@ -986,10 +1006,10 @@ __global__ __launch_bounds__(kSkNT, 1) void scan_small_kernel(const __grid_const
                         tc::fence_after_sync();
                     }
                     const int w = nc - u * kSkUW < kSkUW ? nc - u * kSkUW : kSkUW;
-                    const uint32_t idesc = tc::idesc_i8(kTM, (w + 15) & ~15, /*a_signed=*/true);
+                    const uint32_t idesc = tc::idesc_f8(kTM, (w + 15) & ~15);
                     // B rows [64 u, 64 u + w): 64 rows = 8 swizzle atoms further
                     const uint64_t bdesc = tc::smem_desc_sw128(bbase + (uint32_t)(u * kSkUW * kKC));
-                    tc::mma_i8_ss_chunk(tmem + (uint32_t)(k * kSkUW), adesc, bdesc, idesc, 0u, nks, &accf[k]);
+                    tc::mma_i8_ss_chunk<true>(tmem + (uint32_t)(k * kSkUW), adesc, bdesc, idesc, 0u, nks, &accf[k]);
                 }
                 tc::commit_warp(&aempty[as]);                // the tile's code operand is free
                 if (t == nt - 1) tc::commit_warp(&bfree[b]);  // the item's query operand is free
@@ -1072,7 +1092,7 @@ __global__ __launch_bounds__(kSkNT, 1) void scan_small_kernel(const __grid_const
                                     for (int i2 = 0; i2 < kEC; ++i2) {
                                         if (col0 + i2 < w) {
                                             const ColC cc = colp_get(cb, col0 + i2);
-                                            const float key = rank_key<kLB>(est_of(acc[i2], cc, fac, pcf), epsnq_of(cc), g1);
+                                            const float key = rank_key<kLB>(est_of<true>(acc[i2], cc, fac, pcf), epsnq_of(cc), g1);
                                             const int64_t off = ((int64_t)(uint32_t)cc.pair << 32) | (uint32_t)cc.q;
                                             a.dense_keys[off + v] = f2o(key);
                                         }
@@ -1086,16 +1106,14 @@ __global__ __launch_bounds__(kSkNT, 1) void scan_small_kernel(const __grid_const
                                     // difference of two floats is never -0 when v > U).  Sign bits
                                     // are shifted in from the last column down (one SHF per column).
                                     const float2 pc2 = make_float2(pcf, pcf), nf2 = make_float2(-fac.y, -fac.y);
-                                    const float2 fx2 = make_float2(fac.x, fac.x), mg2 = make_float2(12582912.0f, 12582912.0f);
+                                    const float2 fx2 = make_float2(fac.x, fac.x);
                                     const float4* P0 = reinterpret_cast<const float4*>(cb + (col0 >> 1));
                                     uint32_t neg = 0u;
 #pragma unroll
                                     for (int i2 = kEC - 2; i2 >= 0; i2 -= 2) {
                                         const float4* P = P0 + 2 * i2;
                                         const float4 ab = P[0], ku = P[1];  // (-a0, -a1, b0, b1), (-K0, -K1, U0, U1)
-                                        const float2 ipn = fsub2(make_float2(__int_as_float(0x4B400000 + (int)acc[i2]),
-                                                                             __int_as_float(0x4B400000 + (int)acc[i2 + 1])),
-                                                                 mg2);
+                                        const float2 ipn = make_float2(__uint_as_float(acc[i2]), __uint_as_float(acc[i2 + 1]));
                                         const float2 inner = ffma2(make_float2(ab.z, ab.w), pc2, make_float2(ku.x, ku.y));
                                         const float2 tt = ffma2(make_float2(ab.x, ab.y), ipn, inner);
                                         const float2 vv = ffma2(nf2, tt, fx2);
@@ -1108,13 +1126,13 @@ __global__ __launch_bounds__(kSkNT, 1) void scan_small_kernel(const __grid_const
 #pragma unroll
                                     for (int i2 = 0; i2 < kEC; ++i2) {
                                         const ColC cc = colp_get(cb, col0 + i2);
-                                        const float est = est_of(acc[i2], cc, fac, pcf);
+                                        const float est = est_of<true>(acc[i2], cc, fac, pcf);
                                         const float key = rank_key<kLB>(est, epsnq_of(cc), g1);
                                         if constexpr (kDump) {
                                             if (vok && col0 + i2 < w) {
                                                 const int64_t di = (a.item_off[cc.pair] + (v >> 5)) * 32 + (v & 31);
                                                 if (di < a.dump_cap) {
-                                                    a.dump_ip[di] = -(int)acc[i2];
+                                                    a.dump_ip[di] = (int)-acc_ipn<true>(acc[i2]);
                                                     a.dump_est[di] = est;
                                                 }
                                             }
@@ -1161,7 +1179,7 @@ __global__ __launch_bounds__(kSkNT, 1) void scan_small_kernel(const __grid_const
                                 const uint32_t acci = tc::tmem_ld1(tbase + (uint32_t)(col0 + i2));
                                 if ((bal >> lane) & 1u) {
                                     const ColC cc = colp_get(cb, col0 + i2);
-                                    const float key = rank_key<kLB>(est_of(acci, cc, fac, pcf), epsnq_of(cc), g1);
+                                    const float key = rank_key<kLB>(est_of<true>(acci, cc, fac, pcf), epsnq_of(cc), g1);
                                     const int pos = base + __popc(bal & ((1u << lane) - 1u));
                                     if (pos < a.cap) a.buf[(size_t)cc.q * a.cap + pos] = make_key(key, row);
                                 }
@@ -1185,7 +1203,9 @@ __global__ __launch_bounds__(kSkNT, 1) void scan_small_kernel(const __grid_const
 void expand_codes(rabitq_index* idx, cudaStream_t st) {
     const size_t bytes = (size_t)(idx->nslots + kTM) * 32 * idx->W;
     RQ_CUDA(cudaMalloc(&idx->codes8, bytes));
-    expand_codes_kernel<<<4096, 256, 0, st>>>(idx->codes, idx->nslots, idx->W, reinterpret_cast<uint4*>(idx->codes8));
+    idx->codes8_f8 = idx->W <= 4;  // Dp <= 128: e4m3 operands (.kind::f8f6f4)
+    expand_codes_kernel<<<4096, 256, 0, st>>>(idx->codes, idx->nslots, idx->W, reinterpret_cast<uint4*>(idx->codes8),
+                                              idx->codes8_f8);
     RQ_CHECK_LAUNCH();
 }
 
@@ -1336,7 +1356,7 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         RQ_REQUIRE(cr == CUDA_SUCCESS, RABITQ_ERR_CUDA, "cuTensorMapEncodeTiled (A) failed: " + std::to_string((int)cr));
     }
-    if (ta && a.small && a.Dp <= kKC && !a.full && (!dump || !(retry || dense))) {
+    if (ta && a.small && a.f8 && a.Dp <= kKC && !a.full && (!dump || !(retry || dense))) {
         // small-K scan (Dp <= 128): item table, dynamic scheduler
         RQ_REQUIRE(group_cols(a.Dp, true) == kSkNG && a.items_bound > 0, RABITQ_ERR_INTERNAL,
                    "small-K scan: group width / item bound");
@@ -1375,16 +1395,17 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
                "grouped scan: TMEM / shared-memory plan does not fit");
     const size_t smem = plan.total;
     const int grid = sms;
-#define RQ_IMMA6(LB, DP, RT, DN, TA, FU)                                                                       \
+#define RQ_IMMA6(LB, DP, RT, DN, TA, FU, F8)                                                                   \
     do {                                                                                                        \
-        RQ_CUDA(cudaFuncSetAttribute(scan_imma_kernel<LB, DP, RT, DN, TA, FU>,                                  \
+        RQ_CUDA(cudaFuncSetAttribute(scan_imma_kernel<LB, DP, RT, DN, TA, FU, F8>,                              \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));                  \
-        scan_imma_kernel<LB, DP, RT, DN, TA, FU><<<grid, n_threads(TA), smem, st>>>(tmap, tmapA, a);            \
+        scan_imma_kernel<LB, DP, RT, DN, TA, FU, F8><<<grid, n_threads(TA), smem, st>>>(tmap, tmapA, a);        \
     } while (0)
-#define RQ_IMMA5(LB, DP, RT, DN, TA)                   \
-    do {                                               \
-        if (a.full) RQ_IMMA6(LB, DP, RT, DN, TA, true);  \
-        else RQ_IMMA6(LB, DP, RT, DN, TA, false);        \
+#define RQ_IMMA5(LB, DP, RT, DN, TA)                          \
+    do {                                                      \
+        if (a.full) RQ_IMMA6(LB, DP, RT, DN, TA, true, false);  \
+        else if (a.f8) RQ_IMMA6(LB, DP, RT, DN, TA, false, true); \
+        else RQ_IMMA6(LB, DP, RT, DN, TA, false, false);        \
     } while (0)
 #define RQ_IMMA4(LB, DP, RT, DN)                \
     do {                                        \

@@ -73,6 +73,7 @@ struct ScanArgs {
     const int64_t* dense_off;   // [npairs] offset of each (query, probe) pair within its query
     int full;                   // 1: unquantized query (NEXT-1), 4 digit rows per pair (npairs = rows)
     int small;                  // 1: Dp <= 128 may take the small-K scan (scan_small_kernel)
+    int f8;                     // 1: e4m3 operands (.kind::f8f6f4): Dp <= 128, 4-bit query (codes8 / qbar8 bytes)
     int64_t items_bound;        // upper bound on the grouping's work items (small-K item table)
 };
 

@@ -176,6 +176,18 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N, bool a_signed = fa
            | ((uint32_t)(M >> 4) << 24);   // M / 16
 }
 
+// Instruction descriptor, .kind::f8f6f4 with A = B = e4m3 and an f32 accumulator
+// (dtype 1 at bits 4-5, a/b formats E4M3 = 0), both K-major.
+__host__ __device__ constexpr uint32_t idesc_f8(int M, int N) {
+    return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// idesc of the grouped scan's code x query contraction: e4m3 (kF8) or s8 x u8
+template <bool kF8>
+__host__ __device__ constexpr uint32_t idesc_scan(int M, int N) {
+    return kF8 ? idesc_f8(M, N) : idesc_i8(M, N, /*a_signed=*/true);
+}
+
 // D[tmem] (+)= A[smem] . B[smem]^T, one elected thread issues.
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                        uint32_t accumulate) {
@@ -215,68 +227,80 @@ __device__ __forceinline__ void mma_i8_ts_warp(uint32_t tmem_d, uint32_t tmem_a,
 // nk (1..4) UMMAs of consecutive 32-byte K steps (A: +8 TMEM columns, B
 // descriptor: +2 (32 bytes)) and the commit of `bar`, from a whole warp with one
 // election: the address increments stay inside the asm, so the operands cross
-// to uniform registers once per chunk instead of once per UMMA.
-__device__ __forceinline__ void mma_i8_ts_chunk(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
-                                                uint32_t accumulate, int nk, uint64_t* bar) {
-#define RQ_MMA_HEAD                                   \
-    "{\n\t.reg .pred p, e, t;\n\t"                    \
+// to uniform registers once per chunk instead of once per UMMA.  kF8: the
+// operands are e4m3 bytes (.kind::f8f6f4, f32 accumulator) instead of 8-bit
+// integers (.kind::i8, s32 accumulator).
+#define RQ_KIND_I8 "kind::i8"
+#define RQ_KIND_F8 "kind::f8f6f4"
+#define RQ_MMA_TS_HEAD(K)                                 \
+    "{\n\t.reg .pred p, e, t;\n\t"                        \
     ".reg .b32 a1, a2, a3;\n\t.reg .b64 b1, b2, b3;\n\t" \
-    "setp.ne.b32 p, %4, 0;\n\t"                        \
-    "setp.eq.b32 t, 0, 0;\n\t"                         \
+    "setp.ne.b32 p, %4, 0;\n\t"                          \
+    "setp.eq.b32 t, 0, 0;\n\t"                           \
     "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t" \
     "add.u64 b1, %2, 2;\n\tadd.u64 b2, %2, 4;\n\tadd.u64 b3, %2, 6;\n\t" \
-    "elect.sync _|e, 0xffffffff;\n\t"                  \
-    "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t"
-#define RQ_MMA_K1 "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %3, t;\n\t"
-#define RQ_MMA_K2 "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a2], b2, %3, t;\n\t"
-#define RQ_MMA_K3 "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a3], b3, %3, t;\n\t"
+    "elect.sync _|e, 0xffffffff;\n\t"                    \
+    "@e tcgen05.mma.cta_group::1." K " [%0], [%1], %2, %3, p;\n\t"
+#define RQ_MMA_TS_K1(K) "@e tcgen05.mma.cta_group::1." K " [%0], [a1], b1, %3, t;\n\t"
+#define RQ_MMA_TS_K2(K) "@e tcgen05.mma.cta_group::1." K " [%0], [a2], b2, %3, t;\n\t"
+#define RQ_MMA_TS_K3(K) "@e tcgen05.mma.cta_group::1." K " [%0], [a3], b3, %3, t;\n\t"
+#define RQ_MMA_SS_HEAD(K)                                 \
+    "{\n\t.reg .pred p, e, t;\n\t"                        \
+    ".reg .b64 a1, a2, a3, b1, b2, b3;\n\t"              \
+    "setp.ne.b32 p, %4, 0;\n\t"                          \
+    "setp.eq.b32 t, 0, 0;\n\t"                           \
+    "add.u64 a1, %1, 2;\n\tadd.u64 a2, %1, 4;\n\tadd.u64 a3, %1, 6;\n\t" \
+    "add.u64 b1, %2, 2;\n\tadd.u64 b2, %2, 4;\n\tadd.u64 b3, %2, 6;\n\t" \
+    "elect.sync _|e, 0xffffffff;\n\t"                    \
+    "@e tcgen05.mma.cta_group::1." K " [%0], %1, %2, %3, p;\n\t"
+#define RQ_MMA_SS_K1(K) "@e tcgen05.mma.cta_group::1." K " [%0], a1, b1, %3, t;\n\t"
+#define RQ_MMA_SS_K2(K) "@e tcgen05.mma.cta_group::1." K " [%0], a2, b2, %3, t;\n\t"
+#define RQ_MMA_SS_K3(K) "@e tcgen05.mma.cta_group::1." K " [%0], a3, b3, %3, t;\n\t"
 #define RQ_MMA_TAIL "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t}"
-#define RQ_MMA_ARGS ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(smem_u32(bar)) : "memory"
-    switch (nk) {
-        case 1: asm volatile(RQ_MMA_HEAD RQ_MMA_TAIL RQ_MMA_ARGS); break;
-        case 2: asm volatile(RQ_MMA_HEAD RQ_MMA_K1 RQ_MMA_TAIL RQ_MMA_ARGS); break;
-        case 3: asm volatile(RQ_MMA_HEAD RQ_MMA_K1 RQ_MMA_K2 RQ_MMA_TAIL RQ_MMA_ARGS); break;
-        default: asm volatile(RQ_MMA_HEAD RQ_MMA_K1 RQ_MMA_K2 RQ_MMA_K3 RQ_MMA_TAIL RQ_MMA_ARGS); break;
+#define RQ_MMA_ARGS_TS ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(smem_u32(bar)) : "memory"
+#define RQ_MMA_ARGS_SS ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(smem_u32(bar)) : "memory"
+#define RQ_MMA_SWITCH(HEAD, K1, K2, K3, ARGS, KIND)                                       \
+    switch (nk) {                                                                         \
+        case 1: asm volatile(HEAD(KIND) RQ_MMA_TAIL ARGS); break;                         \
+        case 2: asm volatile(HEAD(KIND) K1(KIND) RQ_MMA_TAIL ARGS); break;                \
+        case 3: asm volatile(HEAD(KIND) K1(KIND) K2(KIND) RQ_MMA_TAIL ARGS); break;       \
+        default: asm volatile(HEAD(KIND) K1(KIND) K2(KIND) K3(KIND) RQ_MMA_TAIL ARGS); break; \
     }
-#undef RQ_MMA_HEAD
-#undef RQ_MMA_K1
-#undef RQ_MMA_K2
-#undef RQ_MMA_K3
-#undef RQ_MMA_TAIL
-#undef RQ_MMA_ARGS
+template <bool kF8 = false>
+__device__ __forceinline__ void mma_i8_ts_chunk(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                                uint32_t accumulate, int nk, uint64_t* bar) {
+    if constexpr (kF8) {
+        RQ_MMA_SWITCH(RQ_MMA_TS_HEAD, RQ_MMA_TS_K1, RQ_MMA_TS_K2, RQ_MMA_TS_K3, RQ_MMA_ARGS_TS, RQ_KIND_F8)
+    } else {
+        RQ_MMA_SWITCH(RQ_MMA_TS_HEAD, RQ_MMA_TS_K1, RQ_MMA_TS_K2, RQ_MMA_TS_K3, RQ_MMA_ARGS_TS, RQ_KIND_I8)
+    }
 }
 
 // The same with A in shared memory too (TMA-written, 128-byte swizzle, K-major):
 // both descriptors advance by 2 (32 bytes) per K step.
+template <bool kF8 = false>
 __device__ __forceinline__ void mma_i8_ss_chunk(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                                 uint32_t accumulate, int nk, uint64_t* bar) {
-#define RQ_MMA_HEAD                                   \
-    "{\n\t.reg .pred p, e, t;\n\t"                    \
-    ".reg .b64 a1, a2, a3, b1, b2, b3;\n\t"            \
-    "setp.ne.b32 p, %4, 0;\n\t"                        \
-    "setp.eq.b32 t, 0, 0;\n\t"                         \
-    "add.u64 a1, %1, 2;\n\tadd.u64 a2, %1, 4;\n\tadd.u64 a3, %1, 6;\n\t" \
-    "add.u64 b1, %2, 2;\n\tadd.u64 b2, %2, 4;\n\tadd.u64 b3, %2, 6;\n\t" \
-    "elect.sync _|e, 0xffffffff;\n\t"                  \
-    "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
-#define RQ_MMA_K1 "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a1, b1, %3, t;\n\t"
-#define RQ_MMA_K2 "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a2, b2, %3, t;\n\t"
-#define RQ_MMA_K3 "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a3, b3, %3, t;\n\t"
-#define RQ_MMA_TAIL "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t}"
-#define RQ_MMA_ARGS ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(smem_u32(bar)) : "memory"
-    switch (nk) {
-        case 1: asm volatile(RQ_MMA_HEAD RQ_MMA_TAIL RQ_MMA_ARGS); break;
-        case 2: asm volatile(RQ_MMA_HEAD RQ_MMA_K1 RQ_MMA_TAIL RQ_MMA_ARGS); break;
-        case 3: asm volatile(RQ_MMA_HEAD RQ_MMA_K1 RQ_MMA_K2 RQ_MMA_TAIL RQ_MMA_ARGS); break;
-        default: asm volatile(RQ_MMA_HEAD RQ_MMA_K1 RQ_MMA_K2 RQ_MMA_K3 RQ_MMA_TAIL RQ_MMA_ARGS); break;
+    if constexpr (kF8) {
+        RQ_MMA_SWITCH(RQ_MMA_SS_HEAD, RQ_MMA_SS_K1, RQ_MMA_SS_K2, RQ_MMA_SS_K3, RQ_MMA_ARGS_SS, RQ_KIND_F8)
+    } else {
+        RQ_MMA_SWITCH(RQ_MMA_SS_HEAD, RQ_MMA_SS_K1, RQ_MMA_SS_K2, RQ_MMA_SS_K3, RQ_MMA_ARGS_SS, RQ_KIND_I8)
     }
-#undef RQ_MMA_HEAD
-#undef RQ_MMA_K1
-#undef RQ_MMA_K2
-#undef RQ_MMA_K3
-#undef RQ_MMA_TAIL
-#undef RQ_MMA_ARGS
 }
+#undef RQ_MMA_SWITCH
+#undef RQ_MMA_ARGS_SS
+#undef RQ_MMA_ARGS_TS
+#undef RQ_MMA_TAIL
+#undef RQ_MMA_SS_K3
+#undef RQ_MMA_SS_K2
+#undef RQ_MMA_SS_K1
+#undef RQ_MMA_SS_HEAD
+#undef RQ_MMA_TS_K3
+#undef RQ_MMA_TS_K2
+#undef RQ_MMA_TS_K1
+#undef RQ_MMA_TS_HEAD
+#undef RQ_KIND_F8
+#undef RQ_KIND_I8
 
 __device__ __forceinline__ void commit_warp(uint64_t* bar) {
     asm volatile(
