@@ -228,7 +228,8 @@ def run_ours(args):
                        profile=prof, rerank=args.rerank, query_bits=args.query_bits, probes=qs_probes)
         elif comm is None:
             idx.search(Q, s.k, s.nprobe, s.M, scan_path=args.scan_path, stream=stream, out=(ids, dist),
-                       profile=prof, rerank=args.rerank, query_bits=args.query_bits)
+                       profile=None if args.graph else prof, rerank=args.rerank, query_bits=args.query_bits,
+                       graph=args.graph)
         else:
             kw = dict(scan_path=args.scan_path, stream=stream.cuda_stream, query_split=args.query_split)
             if prof is not None:
@@ -265,6 +266,12 @@ def run_ours(args):
     torch.cuda.synchronize()
     barrier()
     clocks = clk.stop()
+    if args.graph and comm is None:  # stage times of the same search on the normal (profiled) path
+        prof = rq.Profile()
+        idx.search(Q, s.k, s.nprobe, s.M, scan_path=args.scan_path, stream=stream, out=(ids, dist), profile=prof,
+                   rerank=args.rerank, query_bits=args.query_bits)
+        torch.cuda.synchronize()
+        profs = [prof.as_dict()]
     total = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(total, op=torch.distributed.ReduceOp.MAX)
@@ -279,7 +286,7 @@ def run_ours(args):
     for _ in range(1):
         if comm is None:
             idx.search(Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path, out=(ih, dh), rerank=args.rerank,
-                       query_bits=args.query_bits)
+                       query_bits=args.query_bits, graph=args.graph)
         else:
             comm.search_sharded(idx, Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path, query_split=args.query_split)
     barrier()
@@ -289,7 +296,7 @@ def run_ours(args):
         t0 = time.perf_counter()
         if comm is None:
             idx.search(Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path, out=(ih, dh), rerank=args.rerank,
-                       query_bits=args.query_bits)
+                       query_bits=args.query_bits, graph=args.graph)
         else:
             r = comm.search_sharded(idx, Qh, s.k, s.nprobe, s.M, scan_path=args.scan_path,
                                     query_split=args.query_split)
@@ -385,6 +392,8 @@ def run_ours(args):
                                    else f"list-shards x{world}"),
                    "l2": "flushed between steps (256 MiB write)", "scan_path": args.scan_path,
                    **({"probing": "query-split" if args.query_split else "replicated"} if (proxy or world > 1) else {}),
+                   **({"mode": "latency (CUDA graph per batch, NEXT-2); stage_ms from one profiled normal-path search"}
+                      if args.graph else {}),
                    **({"rerank": "bound-driven (NEXT-4)"} if args.rerank else {}),
                    **({"query": "unquantized, 24-bit fixed point digit rows (NEXT-1)"} if args.query_bits == 32
                       else {})},
@@ -630,6 +639,8 @@ def main():
                     help="1: bound-driven re-rank set (NEXT-4; changes results, opt-in)")
     ap.add_argument("--workload", choices=["search", "build"], default="search",
                     help="build: time rabitq_build (NEXT-3) instead of the search hot path")
+    ap.add_argument("--graph", type=int, default=0, choices=[0, 1],
+                    help="1: latency mode (NEXT-2): the batch captured once as a CUDA graph and replayed")
     ap.add_argument("--query-split", type=int, default=1, choices=[0, 1], dest="query_split",
                     help="N > 1 / --shard: 1 = each rank probes nq/G queries, probe lists all-gathered (SURVEY 8(e))")
     ap.add_argument("--shard", default="", help="r/G: time shard r of G on one GPU (per-GPU proxy for configs "

@@ -171,6 +171,13 @@ typedef struct {
                                 the probe lists are all-gathered (one ncclAllGather of
                                 nq x nprobe int32) -- the probe GEMM is split G ways
                                 (SURVEY 8(e)); results are identical                          */
+    int32_t graph;           /* 1: latency mode for a single-batch call without
+                                debug / profile / rerank / probes_in: the whole path is captured
+                                once as a CUDA graph (no host synchronisation inside; sizes from
+                                host bounds) and replayed per call -- one input copy, one graph
+                                launch, one output copy, one synchronisation; a batch whose
+                                survivor buffers overflowed is re-run on the normal path, so
+                                results are identical.  Graphs are cached per index and shape. */
 } rabitq_search_opts;
 
 /* rabitq_search_opts.variant bits (results are identical with any of them) */

@@ -105,6 +105,7 @@ class SearchOpts(ctypes.Structure):
         ("variant", ctypes.c_uint32),
         ("probes_in", ctypes.c_void_p),
         ("query_split", ctypes.c_int32),
+        ("graph", ctypes.c_int32),
     ]
 
 
@@ -249,7 +250,7 @@ class Index:
                rank_key: int = RANK_EST, eps0: float = 0.0, query_id_base: int = 0, cap: int = 0,
                seed_max: int = 0, stream=None, debug: Optional[dict] = None, out=None,
                profile: Optional[Profile] = None, rerank: int = RERANK_FIXED, query_bits: int = 4,
-               variant: int = 0, probes=None):
+               variant: int = 0, probes=None, graph: int = 0):
         """Returns (ids int64 [nq, k], dists float32 [nq, k]) on Q's device.
         ``debug`` maps rabitq_debug member names to preallocated tensors.
         Device inputs run on ``stream`` (default: torch's current stream)."""
@@ -271,6 +272,7 @@ class Index:
         o.rerank = rerank
         o.query_bits = query_bits
         o.variant = variant
+        o.graph = graph
         if probes is not None:
             probes = probes.contiguous() if hasattr(probes, "contiguous") else np.ascontiguousarray(probes, np.int32)
             o.probes_in = _ptr(probes)

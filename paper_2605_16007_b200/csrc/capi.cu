@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <string>
 #include <cstdlib>
@@ -233,10 +234,14 @@ rabitq_status rabitq_build_ex(const float* X, int64_t n, int32_t d, int32_t nlis
     API_END
 }
 
+static void free_graph_cache(void* p);
+
 void rabitq_free(rabitq_index* idx) {
     if (!idx) return;
     cudaSetDevice(idx->device);
     cudaStreamSynchronize(idx->stream);
+    free_graph_cache(idx->graphs);
+    idx->graphs = nullptr;
     rabitq::free_index_memory(idx);
     cudaStreamDestroy(idx->stream);
     delete idx;
@@ -245,6 +250,101 @@ void rabitq_free(rabitq_index* idx) {
 rabitq_status rabitq_search(const rabitq_index* idx, const float* Q, int64_t nq, int32_t k, int32_t nprobe,
                             int32_t n_rerank, int64_t* ids, float* dists) {
     return rabitq_search_ex(idx, Q, nq, k, nprobe, n_rerank, nullptr, ids, dists);
+}
+
+// ----------------------------------------------------- NEXT-2 latency mode --
+// One batch's whole path captured once as a CUDA graph (latency mode: no host
+// synchronisation inside, SearchCfg::latency) and replayed: per call one copy
+// of Q into the graph's input buffer, one graph launch, one copy out and one
+// synchronisation, at which the batch's overflow / non-finite counters are
+// read; a batch whose survivor buffers overflowed is re-run on the normal path
+// (results never depend on which path ran).  Keyed by every argument that the
+// captured kernels bake in; a small per-index cache.
+struct GraphEntry {
+    int64_t nq = 0, qid_base = 0;
+    int k = 0, nprobe = 0, M = 0;
+    rabitq::SearchCfg cfg;
+    cudaGraphExec_t exec = nullptr;
+    float* Qg = nullptr;
+    int64_t* ids = nullptr;
+    float* d = nullptr;
+    int* flags = nullptr;  // host pinned [8]
+    ~GraphEntry() {
+        if (exec) cudaGraphExecDestroy(exec);
+        cudaFree(Qg);
+        cudaFree(ids);
+        cudaFree(d);
+        cudaFreeHost(flags);
+    }
+};
+struct GraphCache {
+    std::mutex mu;
+    std::vector<std::unique_ptr<GraphEntry>> entries;
+};
+
+static void free_graph_cache(void* p) { delete static_cast<GraphCache*>(p); }
+
+static bool same_cfg(const rabitq::SearchCfg& a, const rabitq::SearchCfg& b) {
+    return a.scan_path == b.scan_path && a.rank_key == b.rank_key && a.eps0 == b.eps0 && a.cap == b.cap &&
+           a.seed_max == b.seed_max && a.refine_rank == b.refine_rank && a.rerank == b.rerank && a.full == b.full &&
+           a.variant == b.variant;
+}
+
+static void search_graph(const rabitq_index* idx, const float* Qd, int64_t nq, int k, int nprobe, int M,
+                         const rabitq::SearchCfg& cfg, int64_t qid_base, int64_t* ids_d, float* d_d, cudaStream_t st) {
+    rabitq_index* mi = const_cast<rabitq_index*>(idx);
+    if (!mi->graphs) mi->graphs = new GraphCache();
+    GraphCache* gc = static_cast<GraphCache*>(mi->graphs);
+    std::lock_guard<std::mutex> lock(gc->mu);  // one replay of an entry at a time (shared I/O buffers)
+    GraphEntry* g = nullptr;
+    for (auto& e : gc->entries)
+        if (e->nq == nq && e->k == k && e->nprobe == nprobe && e->M == M && e->qid_base == qid_base &&
+            same_cfg(e->cfg, cfg))
+            g = e.get();
+    const int D = idx->D;
+    if (!g) {
+        if (gc->entries.size() >= 8) gc->entries.erase(gc->entries.begin());
+        auto e = std::make_unique<GraphEntry>();
+        e->nq = nq, e->k = k, e->nprobe = nprobe, e->M = M, e->qid_base = qid_base, e->cfg = cfg;
+        RQ_CUDA(cudaMalloc(&e->Qg, (size_t)nq * D * sizeof(float)));
+        RQ_CUDA(cudaMalloc(&e->ids, (size_t)nq * k * sizeof(int64_t)));
+        RQ_CUDA(cudaMalloc(&e->d, (size_t)nq * k * sizeof(float)));
+        RQ_CUDA(cudaMallocHost(&e->flags, 8 * sizeof(int)));
+        cudaStream_t cs = nullptr;
+        RQ_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        rabitq::SearchCfg c = cfg;
+        c.latency = true;
+        c.flags_out = e->flags;
+        cudaGraph_t graph = nullptr;
+        RQ_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        try {
+            rabitq::SearchStats stats;
+            rabitq::search_batch(idx, e->Qg, nq, k, nprobe, M, c, qid_base, e->ids, e->d, rabitq::DebugOut{}, cs,
+                                 &stats);
+        } catch (...) {
+            cudaStreamEndCapture(cs, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            cudaStreamDestroy(cs);
+            throw;
+        }
+        RQ_CUDA(cudaStreamEndCapture(cs, &graph));
+        cudaStreamDestroy(cs);
+        const cudaError_t ie = cudaGraphInstantiate(&e->exec, graph, 0);
+        cudaGraphDestroy(graph);
+        RQ_CUDA(ie);
+        g = e.get();
+        gc->entries.push_back(std::move(e));
+    }
+    RQ_CUDA(cudaMemcpyAsync(g->Qg, Qd, (size_t)nq * D * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    RQ_CUDA(cudaGraphLaunch(g->exec, st));
+    RQ_CUDA(cudaMemcpyAsync(ids_d, g->ids, (size_t)nq * k * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    RQ_CUDA(cudaMemcpyAsync(d_d, g->d, (size_t)nq * k * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    RQ_CUDA(cudaStreamSynchronize(st));
+    RQ_REQUIRE(g->flags[0] == 0, RABITQ_ERR_INVALID_DATA, "Q contains non-finite values");
+    if (g->flags[1] != 0) {  // a survivor buffer overflowed / under-filled: the normal path re-scans
+        rabitq::SearchStats stats;
+        rabitq::search_batch(idx, Qd, nq, k, nprobe, M, cfg, qid_base, ids_d, d_d, rabitq::DebugOut{}, st, &stats);
+    }
 }
 
 static void search_local(const rabitq_index* idx, const float* Q, int64_t nq, int k, int nprobe, int M,
@@ -309,6 +409,10 @@ static void search_local(const rabitq_index* idx, const float* Q, int64_t nq, in
         probes_d = (const int32_t*)sp.p;
     }
     if (probes_d && !trusted_probes) rabitq::check_probes(probes_d, (int64_t)nq * nprobe, idx->nlist, st);
+    if (o.graph && qbatch >= nq && !dg && !o.profile && o.rerank == 0 && !probes_d) {
+        search_graph(idx, Qd, nq, k, nprobe, M, cfg, o.query_id_base, ids_d, dists_d, st);
+        return;
+    }
     rabitq::SearchStats stats;
     stats.timing = o.profile != nullptr;
     for (int64_t b0 = 0; b0 < nq; b0 += qbatch) {

@@ -49,6 +49,7 @@ struct rabitq_index {
     bool borrowed = false;
 
     std::vector<int64_t> h_list_off, h_slot_off;
+    void* graphs = nullptr;        // capi.cu: cache of captured latency-mode search graphs (NEXT-2)
 };
 
 namespace rabitq {

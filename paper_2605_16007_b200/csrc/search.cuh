@@ -159,6 +159,11 @@ struct SearchCfg {
     int full = 0;         // 1: unquantized query (NEXT-1), grouped tensor-core scan
     uint32_t variant = 0; // result-invariant execution variants (rabitq_search_opts.variant)
     const int32_t* probes_in = nullptr;  // DEVICE [nq x nprobe]: skip S2-S3 (query-split probing)
+    // latency mode (NEXT-2, CUDA-graph capturable): no host synchronisation -- sizes from host-side
+    // bounds, no side stream, one overflow check whose counters go to `flags_out` (host pinned, 8 ints:
+    // [0] non-finite Q, [1] queries that need a re-scan); the caller re-runs the batch normally if set
+    bool latency = false;
+    int* flags_out = nullptr;
 };
 
 struct DebugOut {  // device-or-host pointers (cudaMemcpyDefault), all nullable

@@ -535,6 +535,38 @@ def test_one_dimension(orc):
     _stage_checks(orc, idx, X, Q, 5, 3, 20)
 
 
+@pytest.mark.parametrize("D,N,nlist,nq,scan_path", [(128, 20000, 64, 64, rq.SCAN_IMMA), (960, 8000, 32, 64, rq.SCAN_AUTO),
+                                                   (128, 20000, 64, 100, rq.SCAN_POPC)])
+def test_graph_latency_mode(D, N, nlist, nq, scan_path):
+    """NEXT-2 latency mode (graph = 1): the batch captured once as a CUDA graph
+    (no host synchronisation inside, sizes from host-side bounds) and replayed
+    gives bit-identical results to the normal path, on repeated calls (graph
+    reuse), with host buffers, and when survivor buffers overflow (the batch is
+    re-run on the normal path); non-finite queries still raise."""
+    X, Q = make_data(D, N, nlist, nq)
+    idx = build(X, nlist)
+    Qd = Q.cuda()
+    base_i, base_d = idx.search(Qd, 10, 8, 100, scan_path=scan_path)
+    for _ in range(3):
+        g_i, g_d = idx.search(Qd, 10, 8, 100, scan_path=scan_path, graph=1)
+        assert torch.equal(g_i, base_i) and torch.equal(g_d, base_d)
+    h_i, h_d = idx.search(Q, 10, 8, 100, scan_path=scan_path, graph=1)
+    assert torch.equal(h_i, base_i.cpu()) and torch.equal(h_d, base_d.cpu())
+    # other queries through the same graph (same shape)
+    Q2 = Qd.flip(0).contiguous()
+    r_i, r_d = idx.search(Q2, 10, 8, 100, scan_path=scan_path)
+    g_i, g_d = idx.search(Q2, 10, 8, 100, scan_path=scan_path, graph=1)
+    assert torch.equal(g_i, r_i) and torch.equal(g_d, r_d)
+    # overflowing survivor buffers: the graph flags the batch, the normal path re-runs it
+    o_i, o_d = idx.search(Qd, 10, 8, 100, scan_path=scan_path, cap=200, seed_max=100, graph=1)
+    assert torch.equal(o_i, base_i) and torch.equal(o_d, base_d)
+    bad = Q.clone()
+    bad[5, 0] = float("nan")
+    with pytest.raises(rq.RabitqError) as e:
+        idx.search(bad.cuda(), 10, 8, 100, scan_path=scan_path, graph=1)
+    assert e.value.status == rq.ERR_INVALID_DATA
+
+
 def test_merge_topk_kernel(orc):
     rng = np.random.default_rng(3)
     G, nq, k = 4, 9, 10
