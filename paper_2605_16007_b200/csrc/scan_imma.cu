@@ -1055,7 +1055,8 @@ __global__ __launch_bounds__(kSkNT, 1) void scan_small_kernel(const __grid_const
             const int s = (int)(i % kSkRI);
             const int nc = R.w & 511, t0 = (int)((uint32_t)R.w >> 13);
             const int x = (int)(uc - u0);
-            const int t = nu == 1 ? x : x / nu, u = x - t * nu;
+            // x / nu for nu in 1..4 without an integer division (x < 32 * 4)
+            const int t = nu == 1 ? x : nu == 2 ? x >> 1 : nu == 4 ? x >> 2 : (x * 43) >> 7, u = x - t * nu;
             const int64_t v = (int64_t)(t0 + t) * kTM + r;
             const bool vok = v < R.y;
             {
