@@ -229,7 +229,7 @@ def run_ours(args):
         elif comm is None:
             idx.search(Q, s.k, s.nprobe, s.M, scan_path=args.scan_path, stream=stream, out=(ids, dist),
                        profile=None if args.graph else prof, rerank=args.rerank, query_bits=args.query_bits,
-                       graph=args.graph)
+                       graph=args.graph, variant=args.variant)
         else:
             kw = dict(scan_path=args.scan_path, stream=stream.cuda_stream, query_split=args.query_split)
             if prof is not None:
@@ -319,6 +319,21 @@ def run_ours(args):
     W = s.W
     scan_bytes = pairs * (4 * W + 8)  # code words + {n_o^2, f1} per (query, vector) pair
     rerank_bytes = s.nq * s.M * (4 * s.D + 8) + surv * 8
+    # with the dense nearest-list block (nq >= 256, slot vectors built: CFG2) the gather kernel moves only
+    # the rows the block cannot decide: use the DRAM bytes ncu measured for it (same workload), not
+    # M (4D + 8) per query, which would read above the HBM peak
+    traffic_all = {}
+    tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{s.cfg}.json")
+    if os.path.exists(tpath):
+        try:
+            traffic_all = json.load(open(tpath))
+        except Exception:
+            traffic_all = {}
+    dense_used = info["bytes_slot_vectors"] > 0 and s.nq >= 256 and s.D % 4 == 0
+    if dense_used and traffic_all.get("select_rerank"):
+        rr_bytes, rr_src = float(traffic_all["select_rerank"]), f"ncu DRAM bytes per launch ({os.path.basename(tpath)})"
+    else:
+        rr_bytes, rr_src = rerank_bytes, "algorithmic M (4D + 8) per query + survivor keys"
     int8_peak = 2.0 * pk.get("bf16_tflops", 1590.0)  # dense int8 = 2x bf16 (nominal ratio, B200_PROFILING.md)
     scan_ops = 2.0 * pairs * s.D  # int8 multiply-adds of <b, qbar>, 2 ops each
     # d <= 128 (the small-K scan): a pair is 4 K-steps of one UMMA but ~5 FP32 lane
@@ -337,9 +352,9 @@ def run_ours(args):
         "scan": ((scan_alu if small_k else scan_tensor) if imma else
                  {"bound": "hbm", "achieved": scan_bytes / (stage_ms["scan"] * 1e-3) / 1e9, "unit": "GB/s",
                   "peak": pk["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs", "algorithmic": scan_bytes}),
-        "select_rerank": {"bound": "hbm", "achieved": rerank_bytes / (stage_ms["select_rerank"] * 1e-3) / 1e9,
+        "select_rerank": {"bound": "hbm", "achieved": rr_bytes / (stage_ms["select_rerank"] * 1e-3) / 1e9,
                           "unit": "GB/s", "peak": pk["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-                          "algorithmic": rerank_bytes},
+                          "algorithmic": rerank_bytes, "bytes_source": rr_src},
     }
     ms_of = {"scan": stage_ms["scan"], "select_rerank": stage_ms["select_rerank"]}
     dom = max(ms_of, key=ms_of.get)
@@ -357,7 +372,8 @@ def run_ours(args):
     other = "select_rerank" if dom == "scan" else "scan"
     ro = rl[other]
     roofline_other = {"kernel": other, "bound": ro["bound"], "achieved": round(ro["achieved"], 1), "unit": ro["unit"],
-                      "frac": round(ro["achieved"] / ro["peak"], 4), "ms": round(ms_of[other], 4)}
+                      "frac": round(ro["achieved"] / ro["peak"], 4), "ms": round(ms_of[other], 4),
+                      **({"bytes_source": ro["bytes_source"]} if "bytes_source" in ro else {})}
     scan_roof = {"path": "tcgen05 int8" if imma else "popc", "pairs": pairs,
                  "hbm_equiv_gbs": round(scan_bytes / (stage_ms["scan"] * 1e-3) / 1e9, 1),
                  "bytes_per_pair": 4 * W + 8, "ms": round(stage_ms["scan"], 4)}
@@ -394,6 +410,7 @@ def run_ours(args):
                    **({"probing": "query-split" if args.query_split else "replicated"} if (proxy or world > 1) else {}),
                    **({"mode": "latency (CUDA graph per batch, NEXT-2); stage_ms from one profiled normal-path search"}
                       if args.graph else {}),
+                   **({"variant": args.variant} if args.variant else {}),
                    **({"rerank": "bound-driven (NEXT-4)"} if args.rerank else {}),
                    **({"query": "unquantized, 24-bit fixed point digit rows (NEXT-1)"} if args.query_bits == 32
                       else {})},
@@ -407,6 +424,10 @@ def run_ours(args):
                         "codes8": info["bytes_codes8"], "slot_vectors": info["bytes_slot_vectors"],
                         "vectors_fp32": s.N * s.D * 4 // max(1, world)},
         "stage_ms": {k_: round(v, 4) for k_, v in stage_ms.items()},
+        **({"dense_rerank_block": {"kernel": "tgemm_dist1 (side stream, beside stages 2-5)",
+                                   "ms": round(float(np.mean([p["dense_ms"] for p in profs])), 4),
+                                   "dram_bytes": traffic_all.get("unnamed>::tgemm_dist1_kernel")}}
+           if float(np.mean([p["dense_ms"] for p in profs])) > 0 else {}),
         "survivors_per_query": round(surv / s.nq, 1), "max_survivors": max_surv, "overflow_rescans": retries,
         **({"reranked_per_query": round(float(np.mean([p["reranked"] for p in profs])) / s.nq, 1)}
            if args.rerank else {}),
@@ -639,6 +660,9 @@ def main():
                     help="1: bound-driven re-rank set (NEXT-4; changes results, opt-in)")
     ap.add_argument("--workload", choices=["search", "build"], default="search",
                     help="build: time rabitq_build (NEXT-3) instead of the search hot path")
+    ap.add_argument("--variant", type=int, default=0,
+                    help="rabitq_search_opts.variant bits (result-invariant paths: 2 = codes expanded in the scan "
+                         "kernel, no expanded-code copy read; 8 = generic grouped scan)")
     ap.add_argument("--graph", type=int, default=0, choices=[0, 1],
                     help="1: latency mode (NEXT-2): the batch captured once as a CUDA graph and replayed")
     ap.add_argument("--query-split", type=int, default=1, choices=[0, 1], dest="query_split",

@@ -132,6 +132,8 @@ typedef struct {
     int32_t scan_path_used;         /* 1 popc, 2 imma                                    */
     int32_t batches;                /* internal query batches                            */
     int64_t reranked;               /* candidates whose exact distance was taken (rerank 1) */
+    float dense_ms;                 /* the dense nearest-list re-rank block (tgemm_dist1), which runs on
+                                       the side stream beside stages 2-5 (not in stage_ms)             */
 } rabitq_profile;
 
 typedef struct {

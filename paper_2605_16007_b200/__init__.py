@@ -81,6 +81,7 @@ class Profile(ctypes.Structure):
         ("scan_path_used", ctypes.c_int32),
         ("batches", ctypes.c_int32),
         ("reranked", ctypes.c_int64),
+        ("dense_ms", ctypes.c_float),
     ]
 
     def as_dict(self):

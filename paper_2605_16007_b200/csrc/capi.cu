@@ -454,6 +454,7 @@ static void search_local(const rabitq_index* idx, const float* Q, int64_t nq, in
         pf->scan_path_used = stats.used_imma ? 2 : 1;
         pf->batches = stats.batches;
         pf->reranked = stats.reranked;
+        pf->dense_ms = stats.dense_ms;
     }
     if (dg) {
         v_qbar.copy_back(st);

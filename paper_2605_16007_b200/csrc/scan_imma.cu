@@ -1109,7 +1109,9 @@ __global__ __launch_bounds__(kSkNT, 1) void scan_small_kernel(const __grid_const
                                     const float2 pc2 = make_float2(pcf, pcf), nf2 = make_float2(-fac.y, -fac.y);
                                     const float2 fx2 = make_float2(fac.x, fac.x);
                                     const float4* P0 = reinterpret_cast<const float4*>(cb + (col0 >> 1));
-                                    uint32_t neg = 0u;
+                                    // two independent shift chains (columns 15..8 and 7..0) so the
+                                    // dependent funnel shifts overlap
+                                    uint32_t neg_hi = 0u, neg_lo = 0u;
 #pragma unroll
                                     for (int i2 = kEC - 2; i2 >= 0; i2 -= 2) {
                                         const float4* P = P0 + 2 * i2;
@@ -1119,10 +1121,11 @@ __global__ __launch_bounds__(kSkNT, 1) void scan_small_kernel(const __grid_const
                                         const float2 tt = ffma2(make_float2(ab.x, ab.y), ipn, inner);
                                         const float2 vv = ffma2(nf2, tt, fx2);
                                         const float2 dd = fsub2(make_float2(ku.z, ku.w), vv);
+                                        uint32_t& neg = i2 >= kEC / 2 ? neg_hi : neg_lo;
                                         neg = __funnelshift_l(__float_as_uint(dd.y), neg, 1);  // (neg << 1) | sign
                                         neg = __funnelshift_l(__float_as_uint(dd.x), neg, 1);
                                     }
-                                    rowbits = ~neg & 0xFFFFu;
+                                    rowbits = ~((neg_hi << (kEC / 2)) | neg_lo) & 0xFFFFu;
                                 } else {
 #pragma unroll
                                     for (int i2 = 0; i2 < kEC; ++i2) {

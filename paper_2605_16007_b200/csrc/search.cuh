@@ -189,6 +189,7 @@ struct SearchStats {
     int64_t max_survivors = 0;
     int retries = 0;
     int64_t reranked = 0;  // rerank 1: candidates re-ranked
+    float dense_ms = 0.f;  // the dense re-rank block (side stream), when timing
     int launches = 0;
     int used_imma = 0;
     int batches = 0;
