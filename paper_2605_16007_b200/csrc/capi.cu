@@ -261,6 +261,7 @@ rabitq_status rabitq_search(const rabitq_index* idx, const float* Q, int64_t nq,
 // (results never depend on which path ran).  Keyed by every argument that the
 // captured kernels bake in; a small per-index cache.
 struct GraphEntry {
+    std::mutex busy;  // held while the entry's graph and I/O buffers are in use (one replay at a time)
     int64_t nq = 0, qid_base = 0;
     int k = 0, nprobe = 0, M = 0;
     rabitq::SearchCfg cfg;
@@ -295,15 +296,33 @@ static void search_graph(const rabitq_index* idx, const float* Qd, int64_t nq, i
     rabitq_index* mi = const_cast<rabitq_index*>(idx);
     if (!mi->graphs) mi->graphs = new GraphCache();
     GraphCache* gc = static_cast<GraphCache*>(mi->graphs);
-    std::lock_guard<std::mutex> lock(gc->mu);  // one replay of an entry at a time (shared I/O buffers)
+    // a free entry of this shape (concurrent callers on other streams take other entries, so
+    // their batches overlap); a new capture when every matching entry is busy
+    std::unique_lock<std::mutex> lock(gc->mu);
     GraphEntry* g = nullptr;
+    std::unique_lock<std::mutex> held;
     for (auto& e : gc->entries)
         if (e->nq == nq && e->k == k && e->nprobe == nprobe && e->M == M && e->qid_base == qid_base &&
-            same_cfg(e->cfg, cfg))
-            g = e.get();
+            same_cfg(e->cfg, cfg)) {
+            std::unique_lock<std::mutex> t(e->busy, std::try_to_lock);
+            if (t.owns_lock()) {
+                g = e.get();
+                held = std::move(t);
+                break;
+            }
+        }
     const int D = idx->D;
     if (!g) {
-        if (gc->entries.size() >= 8) gc->entries.erase(gc->entries.begin());
+        if (gc->entries.size() >= 8) {  // drop the oldest idle entry
+            for (auto it = gc->entries.begin(); it != gc->entries.end(); ++it) {
+                std::unique_lock<std::mutex> t((*it)->busy, std::try_to_lock);
+                if (t.owns_lock()) {
+                    t.unlock();
+                    gc->entries.erase(it);
+                    break;
+                }
+            }
+        }
         auto e = std::make_unique<GraphEntry>();
         e->nq = nq, e->k = k, e->nprobe = nprobe, e->M = M, e->qid_base = qid_base, e->cfg = cfg;
         RQ_CUDA(cudaMalloc(&e->Qg, (size_t)nq * D * sizeof(float)));
@@ -333,8 +352,10 @@ static void search_graph(const rabitq_index* idx, const float* Qd, int64_t nq, i
         cudaGraphDestroy(graph);
         RQ_CUDA(ie);
         g = e.get();
+        held = std::unique_lock<std::mutex>(g->busy);
         gc->entries.push_back(std::move(e));
     }
+    lock.unlock();  // replay under the entry's own lock only
     RQ_CUDA(cudaMemcpyAsync(g->Qg, Qd, (size_t)nq * D * sizeof(float), cudaMemcpyDeviceToDevice, st));
     RQ_CUDA(cudaGraphLaunch(g->exec, st));
     RQ_CUDA(cudaMemcpyAsync(ids_d, g->ids, (size_t)nq * k * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
