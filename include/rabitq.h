@@ -145,8 +145,10 @@ typedef struct {
                                 >= 2 n_rerank; overflowing queries are re-scanned with a tighter
                                 threshold until they fit                                       */
     int32_t seed_max;        /* size of the per-query sample of probed vectors that seeds the
-                                pruning threshold, 0 -> auto (about 20 P / T, capped
-                                at 16384; P = probed vectors, T = target survivors)           */
+                                pruning threshold, 0 -> auto: d <= 128 on the tensor
+                                cores 8192 vectors of the nearest lists; else about 20 P / T,
+                                capped at 16384 (P = probed vectors, T = target survivors).
+                                Results never depend on it                                     */
     void* stream;            /* cudaStream_t to run on (NULL -> the index's stream); outputs
                                 in device memory are valid after that stream synchronizes     */
     rabitq_debug* debug;     /* nullable                                                       */
@@ -189,6 +191,12 @@ typedef struct {
 #define RABITQ_VARIANT_NO_DENSE_RERANK 4u    /* exact gather of every re-rank candidate          */
 #define RABITQ_VARIANT_GENERIC_SCAN 8u       /* d <= 128: the generic grouped scan kernel instead
                                                  of the small-K one                              */
+#define RABITQ_VARIANT_UNIFORM_SEED 16u      /* d <= 128, tensor-core scan: threshold from a uniform
+                                                 prefix sample of every probed list (the d > 128
+                                                 seeding) instead of the nearest lists           */
+#define RABITQ_VARIANT_NO_FOLD 32u           /* d <= 128, tensor-core scan: survivor test on the
+                                                 CUDA cores (scan_small_kernel) instead of the
+                                                 tensor-core folded test                         */
 
 /* Search nq queries Q [nq x d] fp32: rotate, probe the nprobe
  * nearest lists, 4-bit Philox-randomized query quantization per (q, list),

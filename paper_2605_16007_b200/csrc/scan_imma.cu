@@ -716,6 +716,69 @@ __global__ void compact_flagged_kernel(const int* __restrict__ flags, int max_ra
     }
 }
 
+// ------------------------------------------------- folded survivor test
+// (scan_fold_kernel, D <= 128).  For f = fac.y > 0 and a = 2 Delta > 0 the fast
+// test A - f (a ip + b pc - K) <= U  (A = n_o^2, U = tau - ||r_q||^2) is
+//     T = ip + pc y1 + y2 + alpha y3 + beta y4 >= 0,
+//     y1 = b / a, y2 = -K / a, y3 = -1 / a, y4 = U / a (column),
+//     alpha = A / f, beta = 1 / f, pc (row),
+// a sum of rank-1 products: the tensor cores compute E = T - ip as a K = 16
+// tf32 contraction (each factor split hi + lo, the three significant
+// products kept: relative error ~2^-21 per term) into a second accumulator,
+// and the epilogue tests E - acc >= 0 (acc = -ip, exact).  The margins make
+// the test conservative: every pair whose est (scan arithmetic, fp32) is <= tau
+// has T >= c S > 0 in exact arithmetic (S = sum of the terms' magnitudes,
+// c = 2^-16 >> the fp32 / tf32 / accumulation errors), so it is flagged;
+// flagged pairs then get their exact key as before.  Rows with f <= 0 (n_o = 0)
+// and columns without a finite positive a or a finite tau always pass (or, tau
+// = -inf, never): their keys are computed exactly.
+constexpr float kFoldC = 1.52587890625e-05f;  // 2^-16
+constexpr float kFoldBig = 1.8446744073709552e19f;  // 2^64
+// X / BX layout: 16 tf32 per row, canonical K-major without swizzle: row r,
+// 4-float chunk c at (r / 8) 512 + c 128 + (r % 8) 16 bytes
+__device__ __forceinline__ void fold_col_put(float* gext, int64_t g, float y1, float y2, float y3, float y4,
+                                             float pad) {
+    const float y1h = tc::tf32_rna(y1), y2h = tc::tf32_rna(y2), y3h = tc::tf32_rna(y3), y4h = tc::tf32_rna(y4);
+    const float y1l = tc::tf32_rna(__fsub_rn(y1, y1h)), y2l = tc::tf32_rna(__fsub_rn(y2, y2h));
+    const float y3l = tc::tf32_rna(__fsub_rn(y3, y3h)), y4l = tc::tf32_rna(__fsub_rn(y4, y4h));
+    (void)pad;
+    float4* o = reinterpret_cast<float4*>(gext + (g >> 3) * 128 + (g & 7) * 4);
+    o[0] = make_float4(y1h, y1l, y2h, y2l);    // x pc, pc, 1, 1
+    o[8] = make_float4(y3h, y3l, y3h, y4h);    // x alpha_h, alpha_h, alpha_l, beta_h
+    o[16] = make_float4(y4l, y4h, 0.f, 0.f);   // x beta_h, beta_l
+    o[24] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+// fold_col_put(-kFoldBig, ...) puts -2^64 into y1 x pc; a pad / force column
+// uses y2 instead (multiplied by 1 in every row):
+__device__ __forceinline__ void fold_col_const(float* gext, int64_t g, float e) {
+    float4* o = reinterpret_cast<float4*>(gext + (g >> 3) * 128 + (g & 7) * 4);
+    o[0] = make_float4(0.f, 0.f, e, 0.f);
+    o[8] = make_float4(0.f, 0.f, 0.f, 0.f);
+    o[16] = make_float4(0.f, 0.f, 0.f, 0.f);
+    o[24] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+__device__ __forceinline__ void fold_col(float* gext, int64_t g, const ColC& cc, int Dp) {
+    const float a = cc.a, tau = cc.tau;
+    const bool fin = isfinite(a) && isfinite(cc.b) && isfinite(cc.K) && isfinite(cc.nq2);
+    if (tau == -INFINITY) {
+        fold_col_const(gext, g, -kFoldBig);  // nothing is <= -inf
+        return;
+    }
+    if (!(a > 0.f) || !fin || !isfinite(tau)) {
+        fold_col_const(gext, g, kFoldBig);  // every pair is a candidate (exact keys decide)
+        return;
+    }
+    const float ia = __frcp_rn(a);
+    const float y1 = __fmul_rn(cc.b, ia), kp = __fmul_rn(cc.K, ia);
+    const float m = __fmul_rn(kFoldC, __fadd_rn(__fmul_rn(15.f, (float)Dp),
+                                                __fadd_rn(__fmul_rn(2.f * (float)Dp, fabsf(y1)), __fmul_rn(2.f, fabsf(kp)))));
+    const float y2 = __fadd_rn(-kp, m);
+    const float y3 = -__fmul_rn(1.f - kFoldC, ia);
+    const float u = __fadd_rn(__fsub_rn(tau, cc.nq2), __fmul_rn(kFoldC, __fadd_rn(cc.nq2, fabsf(tau))));
+    const float y4 = __fmul_rn(u, ia);
+    fold_col_put(gext, g, y1, y2, y3, y4, 0.f);
+}
+
 // column constants of every grouped row (one half of a 64-byte ColPair record
 // per (query, list) pair; pad rows (gpair < 0) are left untouched: every
 // consumer masks columns past the group's size)
@@ -724,10 +787,14 @@ __global__ void colc_kernel(const int32_t* __restrict__ gpair, int64_t nrows, in
                             const float4* __restrict__ qscal, const float* __restrict__ tau,
                             const uint64_t* __restrict__ tau64, float eps0, const int64_t* __restrict__ dbase,
                             const int64_t* __restrict__ doff, const int32_t* __restrict__ probes,
-                            const float* __restrict__ list_amax, ColPair* __restrict__ gcolp) {
+                            const float* __restrict__ list_amax, ColPair* __restrict__ gcolp,
+                            float* __restrict__ gext, int Dp) {
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < nrows; g += (int64_t)gridDim.x * blockDim.x) {
         const int p = gpair[g];
-        if (p < 0) continue;
+        if (p < 0) {
+            if (gext) fold_col_const(gext, g, -kFoldBig);  // pad column: never a survivor
+            continue;
+        }
         const int q = p / nprobe;
         const PairC pc = pair_consts(qscal[p], D);
         ColC cc;
@@ -758,6 +825,7 @@ __global__ void colc_kernel(const int32_t* __restrict__ gpair, int64_t nrows, in
             cc.U = __fadd_rn(__fsub_rn(cc.tau, pc.nq2), __fmul_rn(4.76837158e-7f, mag));  // 2^-21
         }
         colp_put(gcolp, (int)g, cc);
+        if (gext) fold_col(gext, g, cc, Dp);
     }
 }
 
@@ -1202,6 +1270,372 @@ __global__ __launch_bounds__(kSkNT, 1) void scan_small_kernel(const __grid_const
     if (warp == 2) tc::tmem_dealloc(tmem, kTmemCols);
 }
 
+// --------------------------------------------------- folded small-K scan
+// Dp <= 128 main scan (est key, no dump): the survivor test runs on the
+// tensor cores (fold_col above).  Per unit (tile, <= 64 group columns) the MMA
+// warp issues the code x query contraction into the ip accumulator and the
+// K = 16 tf32 contraction of the row / column factors into the E accumulator
+// of the same TMEM slot (4 slots of 2 x 64 columns); the epilogue loads both,
+// E - acc per pair (packed FP32), ANDs the 16 results of a chunk and takes the
+// slow path (exact keys, the small kernel's survivor appends) only when a sign
+// bit is clear somewhere in the warp.  A stages carry the tile's codes (TMA)
+// and its X rows (16 tf32 per vector, written by a producer warp from the
+// tile's row constants); row constants live in a per-tile ring, released when
+// every unit of the tile is done, so the A loader runs ahead of the MMA by the
+// A stages alone.
+constexpr int kFxUW = 64;                   // unit width
+constexpr int kFxUS = 4;                    // TMEM slots: ip [64] + E [64] columns each
+constexpr int kFxSA = 4;                    // A stages (codes 16 KB + X 8 KB)
+constexpr int kFxRT = 8;                    // row-constant ring (tiles)
+constexpr int kFxRI = 6;                    // item records
+constexpr int kFxEpiW = 12;                 // epilogue warps (3 per TMEM lane quarter)
+constexpr int kFxXW = 4;                    // X producer warps (one vector row per lane)
+constexpr int kFxMmaW = 2 + kFxXW;          // warps 0 sched + B, 1 A loader, 2..5 X producers, 6 MMA
+constexpr int kFxEpi0 = kFxMmaW + 1;
+constexpr int kFxNT = (kFxEpi0 + kFxEpiW) * 32;  // 608 threads
+constexpr uint32_t kFxBStage = kSkNG * kKC;      // 32 KB query operand
+constexpr uint32_t kFxBXStage = kSkNG * 64;      // 16 KB column factors (16 tf32 per column)
+constexpr uint32_t kFxXStage = kTM * 64;         // 8 KB row factors
+constexpr uint32_t kFxAStage = kAStage + kFxXStage;  // 24 KB
+constexpr uint32_t kFxOffBX = 2 * kFxBStage;
+constexpr uint32_t kFxOffA = kFxOffBX + 2 * kFxBXStage;  // multiple of 1024
+constexpr uint32_t kFxOffR = kFxOffA + kFxSA * kFxAStage;
+constexpr uint32_t kFxSmem = kFxOffR + kFxRT * sizeof(SkRows) + 1024;
+static_assert(kFxSmem <= 227 * 1024, "fold scan shared memory");
+static_assert(kFxOffA % 1024 == 0 && kFxAStage % 1024 == 0, "A stages 1024-aligned (128-byte swizzle)");
+
+template <int NK>
+__global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_constant__ CUtensorMap tmapB,
+                                                             const __grid_constant__ CUtensorMap tmapA, ScanArgs a,
+                                                             const float* __restrict__ gext,
+                                                             const int4* __restrict__ items, int* __restrict__ sched) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
+    uint8_t* smem = smem_raw + pad;  // [2] B | [2] BX | [kFxSA] (codes | X) | [kFxRT] row constants
+    SkRows* urows = reinterpret_cast<SkRows*>(smem + kFxOffR);
+    __shared__ int4 rec[kFxRI];
+    __shared__ uint32_t next_unit[4];
+    __shared__ __align__(8) uint64_t ifull[kFxRI], iempty[kFxRI], bfull[2], bfree[2], afull[kFxSA], xfull[kFxSA],
+        aempty[kFxSA], accf[kFxUS], acce[kFxUS], rowf[kFxRT], rempty[kFxRT];
+    __shared__ uint32_t tmem_base_s;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (warp == kFxMmaW) tc::tmem_alloc(&tmem_base_s, kTmemCols);
+    if (tid == 0) {
+        for (int s = 0; s < kFxRI; ++s) {
+            tc::mbar_init(&ifull[s], 1);
+            tc::mbar_init(&iempty[s], 2 + kFxXW + kFxEpiW);  // A loader, X producers, MMA warp, epilogue warps
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&bfull[b], 1);
+            tc::mbar_init(&bfree[b], 1);
+        }
+        for (int s = 0; s < kFxSA; ++s) {
+            tc::mbar_init(&afull[s], 1);
+            tc::mbar_init(&xfull[s], kFxXW);
+            tc::mbar_init(&aempty[s], 1);
+        }
+        for (int k = 0; k < kFxUS; ++k) {
+            tc::mbar_init(&accf[k], 1);
+            tc::mbar_init(&acce[k], 4);  // one warp per TMEM lane quarter
+        }
+        for (int t = 0; t < kFxRT; ++t) {
+            tc::mbar_init(&rowf[t], 1);
+            tc::mbar_init(&rempty[t], 48);  // 4 quarters x nu units x 12 / nu
+        }
+        for (int q = 0; q < 4; ++q) next_unit[q] = 0u;
+        tc::prefetch_tmap(&tmapB);
+        tc::prefetch_tmap(&tmapA);
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = tmem_base_s;
+    const int64_t nitems = a.list_items[a.nlist];
+
+    if (warp == 0) {
+        // ============ scheduler: item records, query operand (B) and column factors (BX) ============
+        if (lane == 0) {
+            for (uint32_t i = 0;; ++i) {
+                const int s = (int)(i % kFxRI);
+                if (i >= (uint32_t)kFxRI) tc::mbar_wait(&iempty[s], ((i / kFxRI) - 1) & 1);
+                const int64_t id = atomicAdd(sched, 1);
+                if (id >= nitems) {
+                    rec[s] = make_int4(0, 0, 0, 0);
+                    tc::mbar_arrive(&ifull[s]);
+                    break;
+                }
+                const int4 r = __ldg(items + id);
+                rec[s] = r;
+                tc::mbar_arrive(&ifull[s]);
+                const int nc = r.w & 511;
+                const int b = (int)(i & 1u);
+                if (i >= 2) tc::mbar_wait(&bfree[b], ((i >> 1) - 1) & 1);
+                const int nb = (nc + kBoxRows - 1) / kBoxRows;
+                const uint32_t bxb = (uint32_t)(nb * kBoxRows) * 64u;
+                tc::mbar_arrive_expect_tx(&bfull[b], (uint32_t)(nb * kBoxRows * kKC) + bxb);
+                for (int bx = 0; bx < nb; ++bx)
+                    tc::tma_load_2d(smem + b * kFxBStage + bx * kBoxRows * kKC, &tmapB, &bfull[b], 0,
+                                    r.z + bx * kBoxRows);
+                tc::bulk_load(smem + kFxOffBX + b * kFxBXStage, gext + (int64_t)r.z * 16, bxb, &bfull[b]);
+            }
+        }
+    } else if (warp == 1) {
+        // ============ code operand (A) by TMA + the tile's row constants ============
+        if (lane == 0) {
+            uint32_t tcnt = 0;
+            for (uint32_t i = 0;; ++i) {
+                const int s = (int)(i % kFxRI);
+                tc::mbar_wait(&ifull[s], (i / kFxRI) & 1);
+                const int4 r = rec[s];
+                tc::mbar_arrive(&iempty[s]);
+                if (r.w == 0) break;
+                const int nt = (r.w >> 9) & 15, t0 = (int)((uint32_t)r.w >> 13);
+                for (int t = 0; t < nt; ++t, ++tcnt) {
+                    const int st = (int)(tcnt % kFxSA);
+                    if (tcnt >= (uint32_t)kFxSA) tc::mbar_wait(&aempty[st], ((tcnt / kFxSA) - 1) & 1);
+                    tc::mbar_arrive_expect_tx(&afull[st], (uint32_t)kAStage);
+                    tc::tma_load_2d(smem + kFxOffA + st * kFxAStage, &tmapA, &afull[st], 0, r.x + (t0 + t) * kTM);
+                    const int rt = (int)(tcnt % kFxRT);
+                    if (tcnt >= (uint32_t)kFxRT) tc::mbar_wait(&rempty[rt], ((tcnt / kFxRT) - 1) & 1);
+                    const int v0 = (t0 + t) * kTM;
+                    const int nv = r.y - v0 < kTM ? r.y - v0 : kTM;
+                    const uint32_t ncp = (uint32_t)((nv + 31) & ~31);
+                    const int64_t s0 = (int64_t)r.x + v0;
+                    SkRows& R = urows[rt];
+                    tc::mbar_arrive_expect_tx(&rowf[rt], ncp * 14u);
+                    tc::bulk_load(R.fac, a.fac + s0, ncp * 8u, &rowf[rt]);
+                    tc::bulk_load(R.pcnt, a.pcnt + s0, ncp * 2u, &rowf[rt]);
+                    tc::bulk_load(R.rows, a.rows + s0, ncp * 4u, &rowf[rt]);
+                }
+            }
+        }
+    } else if (warp < kFxMmaW) {
+        // ============ X producers: 16 tf32 row factors per vector of each tile ============
+        uint32_t tcnt = 0;
+        for (uint32_t i = 0;; ++i) {
+            const int s = (int)(i % kFxRI);
+            tc::mbar_wait(&ifull[s], (i / kFxRI) & 1);
+            const int4 r = rec[s];
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&iempty[s]);
+            if (r.w == 0) break;
+            const int nt = (r.w >> 9) & 15, t0 = (int)((uint32_t)r.w >> 13);
+            for (int t = 0; t < nt; ++t, ++tcnt) {
+                const int st = (int)(tcnt % kFxSA), rt = (int)(tcnt % kFxRT);
+                if (tcnt >= (uint32_t)kFxSA) tc::mbar_wait(&aempty[st], ((tcnt / kFxSA) - 1) & 1);
+                tc::mbar_wait(&rowf[rt], (tcnt / kFxRT) & 1);
+                const SkRows& R = urows[rt];
+                uint8_t* xs = smem + kFxOffA + st * kFxAStage + kAStage;
+                const int nv = r.y - (t0 + t) * kTM;
+                {
+                    const int rr = (warp - 2) * 32 + lane;
+                    float pc = 0.f, ah = 0.f, al = 0.f, bh = 0.f, bl = 0.f;
+                    if (rr < nv) {
+                        const float2 fc = R.fac[rr];
+                        pc = (float)R.pcnt[rr];
+                        const float beta = __frcp_rn(fc.y), alpha = __fmul_rn(fc.x, beta);
+                        if (fc.y > 0.f && isfinite(beta) && isfinite(alpha)) {
+                            ah = tc::tf32_rna(alpha);
+                            al = tc::tf32_rna(__fsub_rn(alpha, ah));
+                            bh = tc::tf32_rna(beta);
+                            bl = tc::tf32_rna(__fsub_rn(beta, bh));
+                        } else {
+                            ah = -kFoldBig;  // f = 0 (n_o = 0): always a candidate
+                        }
+                    }
+                    float4* o = reinterpret_cast<float4*>(xs + (rr >> 3) * 512 + (rr & 7) * 16);
+                    o[0] = make_float4(pc, pc, 1.f, 1.f);
+                    o[8] = make_float4(ah, ah, al, bh);
+                    o[16] = make_float4(bh, bl, 0.f, 0.f);
+                    o[24] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+                tc::fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&xfull[st]);
+            }
+        }
+    } else if (warp == kFxMmaW) {
+        // ============ MMA issuer (one thread): per unit the ip and E contractions into slot ucnt % 4 ============
+        if (lane == 0) {
+            uint32_t tcnt = 0, ucnt = 0;
+            const uint32_t accf_s = tc::smem_u32(accf), acce_s = tc::smem_u32(acce);
+            for (uint32_t i = 0;; ++i) {
+                const int s = (int)(i % kFxRI);
+                tc::mbar_wait(&ifull[s], (i / kFxRI) & 1);
+                const int4 r = rec[s];
+                tc::mbar_arrive(&iempty[s]);
+                if (r.w == 0) break;
+                const int nc = r.w & 511, nt = (r.w >> 9) & 15;
+                const int nu = (nc + kFxUW - 1) / kFxUW;
+                const int wl = nc - (nu - 1) * kFxUW;  // width of the last unit
+                const uint32_t id8 = tc::idesc_f8(kTM, kFxUW), id32 = tc::idesc_tf32_f32(kTM, kFxUW);
+                const uint32_t id8l = tc::idesc_f8(kTM, (wl + 15) & ~15), id32l = tc::idesc_tf32_f32(kTM, (wl + 15) & ~15);
+                const int b = (int)(i & 1u);
+                tc::mbar_wait(&bfull[b], (i >> 1) & 1);
+                tc::fence_after_sync();
+                const uint64_t bdesc0 = tc::smem_desc_sw128(tc::smem_u32(smem + b * kFxBStage));
+                const uint64_t bxdesc0 = tc::smem_desc(tc::smem_u32(smem + kFxOffBX + b * kFxBXStage), 128, 512);
+#pragma unroll 1
+                for (int t = 0; t < nt; ++t, ++tcnt) {
+                    const int as = (int)(tcnt % kFxSA);
+                    tc::mbar_wait(&afull[as], (tcnt / kFxSA) & 1);
+                    tc::mbar_wait(&xfull[as], (tcnt / kFxSA) & 1);
+                    tc::fence_after_sync();
+                    const uint32_t abase = tc::smem_u32(smem + kFxOffA + as * kFxAStage);
+                    const uint64_t adesc = tc::smem_desc_sw128(abase);
+                    const uint64_t xdesc = tc::smem_desc(abase + kAStage, 128, 512);
+#pragma unroll 1
+                    for (int u = 0; u < nu; ++u, ++ucnt) {
+                        const uint32_t k = ucnt % kFxUS;
+                        if (ucnt >= (uint32_t)kFxUS) {
+                            tc::mbar_wait_s(acce_s + 8u * k, ((ucnt / kFxUS) - 1) & 1);
+                            tc::fence_after_sync();
+                        }
+                        const bool last = u == nu - 1;
+                        // B rows [64 u, +64): 8 KB = 512 descriptor units (SW128); BX: 4 KB = 256
+                        tc::mma_fold_unit1<NK>(tmem + k * 128u, tmem + k * 128u + 64u, adesc,
+                                               bdesc0 + (uint64_t)(u * 512), last ? id8l : id8, xdesc,
+                                               bxdesc0 + (uint64_t)(u * 256), last ? id32l : id32, accf_s + 8u * k);
+                    }
+                    tc::commit(&aempty[as]);                // the tile's codes and X rows are free
+                    if (t == nt - 1) tc::commit(&bfree[b]);  // the item's B and BX are free
+                }
+            }
+        }
+    } else {
+        // ============ epilogue: 32 rows (the warp's lane quarter) x a unit's columns ============
+        const int quarter = warp & 3;
+        const int r = quarter * 32 + lane;
+        const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+        const uint32_t rowf_s = tc::smem_u32(rowf), accf_s = tc::smem_u32(accf), acce_s = tc::smem_u32(acce),
+                       rempty_s = tc::smem_u32(rempty);
+        uint32_t i = 0, u0 = 0, tc0 = 0;  // item cursor, its first unit and first tile
+        int4 R = make_int4(0, 0, 0, 0);
+        int nu = 0, nut = -1;
+        for (;;) {
+            uint32_t uc = 0;
+            if (lane == 0) uc = atomicAdd(&next_unit[quarter], 1u);
+            uc = __shfl_sync(0xFFFFFFFFu, uc, 0);
+            bool done = false;
+            for (;;) {
+                if (nut < 0) {
+                    tc::mbar_wait(&ifull[i % kFxRI], (i / kFxRI) & 1);
+                    R = rec[i % kFxRI];
+                    if (R.w == 0) {
+                        done = true;
+                        break;
+                    }
+                    nu = ((R.w & 511) + kFxUW - 1) / kFxUW;
+                    nut = ((R.w >> 9) & 15) * nu;
+                }
+                if (uc < u0 + (uint32_t)nut) break;
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&iempty[i % kFxRI]);
+                u0 += (uint32_t)nut;
+                tc0 += (uint32_t)(((R.w >> 9) & 15));
+                ++i;
+                nut = -1;
+            }
+            if (done) break;
+            const int nc = R.w & 511, t0 = (int)((uint32_t)R.w >> 13);
+            const int x = (int)(uc - u0);
+            const int t = nu == 1 ? x : nu == 2 ? x >> 1 : nu == 4 ? x >> 2 : (x * 43) >> 7, u = x - t * nu;
+            const int64_t v = (int64_t)(t0 + t) * kTM + r;
+            const bool vok = v < R.y;
+            const uint32_t tcnt = tc0 + (uint32_t)t;
+            const int rt = (int)(tcnt % kFxRT);
+            const int k = (int)(uc % kFxUS);
+            const uint32_t ph = (uc / kFxUS) & 1;
+            const int w = nc - u * kFxUW < kFxUW ? nc - u * kFxUW : kFxUW;
+            const int64_t gcol0 = (int64_t)R.z + u * kFxUW;  // grouped row of the unit's column 0
+            tc::mbar_wait_s(accf_s + 8u * k, ph);
+            tc::fence_after_sync();
+            const uint32_t tbase = lane_base + (uint32_t)(k * 128);
+            bool rows_ready = false;
+#pragma unroll
+            for (int h = 0; h < kFxUW / kEC; ++h) {
+                const int col0 = h * kEC;
+                if (col0 >= w) break;
+                uint32_t acc[kEC], ev[kEC];
+                tc::tmem_ld16_nw(tbase + (uint32_t)col0, acc);
+                tc::tmem_ld16_nw(tbase + 64u + (uint32_t)col0, ev);
+                tc::tmem_ld_wait();
+                uint32_t dbits[kEC];
+#pragma unroll
+                for (int c = 0; c < kEC; c += 2) {
+                    const float2 dd = fsub2(make_float2(__uint_as_float(ev[c]), __uint_as_float(ev[c + 1])),
+                                            make_float2(__uint_as_float(acc[c]), __uint_as_float(acc[c + 1])));
+                    dbits[c] = __float_as_uint(dd.x);
+                    dbits[c + 1] = __float_as_uint(dd.y);
+                }
+                uint32_t all = dbits[0];
+#pragma unroll
+                for (int c = 1; c < kEC; ++c) all &= dbits[c];
+                const bool cand = vok && !(all >> 31);
+                if (!__any_sync(0xFFFFFFFFu, cand)) continue;
+                // ---- slow path: exact keys of the flagged pairs of this chunk ----
+                if (!rows_ready) {
+                    tc::mbar_wait_s(rowf_s + 8u * rt, (tcnt / kFxRT) & 1);
+                    rows_ready = true;
+                }
+                const SkRows& RS = urows[rt];
+                const float2 fac = vok ? RS.fac[r] : make_float2(0.f, 0.f);
+                const float pcf = vok ? (float)RS.pcnt[r] : 0.f;
+                const uint32_t row = vok ? RS.rows[r] : 0u;
+                uint32_t rowbits = 0u;
+#pragma unroll
+                for (int c = kEC - 1; c >= 0; --c) rowbits = (rowbits << 1) | (1u - (dbits[c] >> 31));
+                const int rem = w - col0;
+                if (rem < kEC) rowbits &= (1u << rem) - 1u;
+                if (!vok) rowbits = 0u;
+                const uint32_t cols = __reduce_or_sync(0xFFFFFFFFu, rowbits);
+                // lane c < 16 owns column c: its row ballot, constants and counter atomic
+                // (one round trip each for all flagged columns of the chunk)
+                uint32_t mybal = 0u;
+                for (uint32_t m = cols; m; m &= m - 1) {
+                    const int i2 = __ffs(m) - 1;
+                    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, (rowbits >> i2) & 1u);
+                    if (lane == i2) mybal = bal;
+                }
+                ColC mc{};
+                int mybase = 0;
+                if (mybal) {
+                    mc = colp_get(a.gcolp, (int)(gcol0 + col0 + lane));
+                    mybase = atomicAdd(&a.cnt[mc.q], __popc(mybal));
+                }
+                for (uint32_t m = cols; m; m &= m - 1) {
+                    const int i2 = __ffs(m) - 1;
+                    const uint32_t bal = __shfl_sync(0xFFFFFFFFu, mybal, i2);
+                    const int base = __shfl_sync(0xFFFFFFFFu, mybase, i2);
+                    ColC cc;
+                    cc.a = __shfl_sync(0xFFFFFFFFu, mc.a, i2);
+                    cc.b = __shfl_sync(0xFFFFFFFFu, mc.b, i2);
+                    cc.K = __shfl_sync(0xFFFFFFFFu, mc.K, i2);
+                    cc.nq2 = __shfl_sync(0xFFFFFFFFu, mc.nq2, i2);
+                    cc.q = __shfl_sync(0xFFFFFFFFu, mc.q, i2);
+                    if ((bal >> lane) & 1u) {
+                        uint32_t accv = acc[0];
+#pragma unroll
+                        for (int c = 1; c < kEC; ++c) accv = (c == i2) ? acc[c] : accv;
+                        const float key = est_of<true>(accv, cc, fac, pcf);
+                        const int pos = base + __popc(bal & ((1u << lane) - 1u));
+                        if (pos < a.cap) a.buf[(size_t)cc.q * a.cap + pos] = make_key(key, row);
+                    }
+                }
+            }
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) {
+                tc::mbar_arrive_s(acce_s + 8u * k);
+                tc::mbar_arrive_cnt_s(rempty_s + 8u * rt, (uint32_t)(12 / nu));
+            }
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == kFxMmaW) tc::tmem_dealloc(tmem, kTmemCols);
+}
+
 }  // namespace
 
 void expand_codes(rabitq_index* idx, cudaStream_t st) {
@@ -1330,9 +1764,14 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
     ScanArgs a = a_in;  // a.nrows = grouped rows allocated (all pairs, or the re-scan's sub list)
     WBuf<ColPair> gcolp;
     gcolp.alloc((size_t)(a.nrows + 1) / 2 + kTN, st);
+    // folded survivor test (scan_fold_kernel): the main est-key scan of the small-K path
+    const bool small_k = a.codes8 != nullptr && a.small && a.f8 && a.Dp <= kKC && !a.full;
+    const bool fold = small_k && a.fold && !lb && !dump && !retry && !dense;
+    WBuf<float> gext;
+    if (fold) gext.alloc(((size_t)a.nrows + 8) * 16, st);
     colc_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((a.nrows + 255) / 256, 2048)), 256, 0, st>>>(
         a.gpair, a.nrows, a.nprobe, a.D, a.qscal, a.tau, retry ? a.tau64 : nullptr, a.eps0,
-        dense ? a.dense_base : nullptr, dense ? a.dense_off : nullptr, a.probes, a.list_amax, gcolp.p);
+        dense ? a.dense_base : nullptr, dense ? a.dense_off : nullptr, a.probes, a.list_amax, gcolp.p, gext.p, a.Dp);
     RQ_CHECK_LAUNCH();
     a.gcolp = gcolp.p;
     int dev = 0, sms = 148;
@@ -1372,6 +1811,23 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
         item_table_kernel<<<(unsigned)std::max(1, std::min(a.nlist, 8192) / 8), 256, 0, st>>>(
             a.nlist, a.list_off, a.slot_off, a.gstart, a.gcount, a.list_items, items.p);
         RQ_CHECK_LAUNCH();
+        if (fold) {
+#define RQ_FOLD(NK)                                                                                          \
+    do {                                                                                                       \
+        RQ_CUDA(cudaFuncSetAttribute(scan_fold_kernel<NK>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                                     (int)kFxSmem));                                                           \
+        scan_fold_kernel<NK><<<sms, kFxNT, kFxSmem, st>>>(tmap, tmapA, a, gext.p, items.p, sched.p);          \
+    } while (0)
+            switch (a.Dp / 32) {
+                case 1: RQ_FOLD(1); break;
+                case 2: RQ_FOLD(2); break;
+                case 3: RQ_FOLD(3); break;
+                default: RQ_FOLD(4); break;
+            }
+#undef RQ_FOLD
+            RQ_CHECK_LAUNCH();
+            return;
+        }
 #define RQ_SMALL(LB, MODE, DP)                                                                                 \
     do {                                                                                                        \
         RQ_CUDA(cudaFuncSetAttribute(scan_small_kernel<LB, MODE, DP>,                                           \

@@ -75,6 +75,7 @@ struct ScanArgs {
     int small;                  // 1: Dp <= 128 may take the small-K scan (scan_small_kernel)
     int f8;                     // 1: e4m3 operands (.kind::f8f6f4): Dp <= 128, 4-bit query (codes8 / qbar8 bytes)
     int64_t items_bound;        // upper bound on the grouping's work items (small-K item table)
+    int fold;                   // 1: the small-K main scan tests survivors on the tensor cores (scan_fold_kernel)
 };
 
 template <typename T>

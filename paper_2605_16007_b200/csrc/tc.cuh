@@ -369,5 +369,91 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// 32 lanes x 16 columns of 32-bit from TMEM without waiting (tmem_ld_wait()
+// before the registers are read)
+__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// arrive on an mbarrier with an arrival count
+__device__ __forceinline__ void mbar_arrive_cnt_s(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+// One unit of the folded scan, from a whole warp with one election:
+//   D_ip = A_codes . B_query^T over nk 32-byte K steps (.kind::f8f6f4, e4m3),
+//   D_e  = X . BX^T over K = 16 tf32 (two UMMAs of K = 8, canonical K-major
+//          layout without swizzle: LBO = 128 B, SBO = 512 B, +256 B per UMMA),
+// then one commit of `bar` (both accumulators complete).
+__device__ __forceinline__ void mma_fold_unit(uint32_t tmem_ip, uint32_t tmem_e, uint64_t adesc, uint64_t bdesc,
+                                              uint32_t idesc8, int nk, uint64_t xdesc, uint64_t bxdesc,
+                                              uint32_t idesc32, uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e, t, p1, p2, p3;\n\t"
+        ".reg .b64 a1, a2, a3, b1, b2, b3, x1, y1;\n\t"
+        "setp.eq.b32 t, 0, 0;\n\t"
+        "setp.gt.s32 p1, %5, 1;\n\tsetp.gt.s32 p2, %5, 2;\n\tsetp.gt.s32 p3, %5, 3;\n\t"
+        "add.u64 a1, %2, 2;\n\tadd.u64 a2, %2, 4;\n\tadd.u64 a3, %2, 6;\n\t"
+        "add.u64 b1, %3, 2;\n\tadd.u64 b2, %3, 4;\n\tadd.u64 b3, %3, 6;\n\t"
+        "add.u64 x1, %6, 16;\n\tadd.u64 y1, %7, 16;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %2, %3, %4, !t;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], %6, %7, %8, !t;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], x1, y1, %8, t;\n\t"
+        "and.pred p1, p1, e;\n\tand.pred p2, p2, e;\n\tand.pred p3, p3, e;\n\t"
+        "@p1 tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a1, b1, %4, t;\n\t"
+        "@p2 tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a2, b2, %4, t;\n\t"
+        "@p3 tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a3, b3, %4, t;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%9];\n\t}" ::"r"(tmem_ip),
+        "r"(tmem_e), "l"(adesc), "l"(bdesc), "r"(idesc8), "r"(nk), "l"(xdesc), "l"(bxdesc), "r"(idesc32),
+        "r"(smem_u32(bar))
+        : "memory");
+}
+
+// The same issued by a single thread (no election), NK = 1..4 K steps of the
+// ip contraction known at compile time.
+template <int NK>
+__device__ __forceinline__ void mma_fold_unit1(uint32_t tmem_ip, uint32_t tmem_e, uint64_t adesc, uint64_t bdesc,
+                                               uint32_t idesc8, uint64_t xdesc, uint64_t bxdesc, uint32_t idesc32,
+                                               uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .pred t;\n\t"
+        ".reg .b64 a1, b1, x1, y1;\n\t"
+        "setp.eq.b32 t, 0, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %2, %3, %4, !t;\n\t"
+        "add.u64 x1, %5, 16;\n\tadd.u64 y1, %6, 16;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%1], %5, %6, %7, !t;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%1], x1, y1, %7, t;\n\t}" ::"r"(tmem_ip),
+        "r"(tmem_e), "l"(adesc), "l"(bdesc), "r"(idesc8), "l"(xdesc), "l"(bxdesc), "r"(idesc32)
+        : "memory");
+#pragma unroll
+    for (int k = 1; k < NK; ++k) {
+        asm volatile(
+            "{\n\t.reg .pred t;\n\tsetp.eq.b32 t, 0, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, t;\n\t}" ::"r"(tmem_ip),
+            "l"(adesc + (uint64_t)(2 * k)), "l"(bdesc + (uint64_t)(2 * k)), "r"(idesc8)
+            : "memory");
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+__host__ __device__ constexpr uint32_t idesc_tf32_f32(int M, int N) {
+    return (1u << 4)                 // c_format: F32
+           | (2u << 7) | (2u << 10)  // a/b format: TF32
+           | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
 }  // namespace tc
 }  // namespace rabitq

@@ -359,23 +359,85 @@ def test_fullq_parity(orc, D, N, nlist, nq, nprobe, k, M):
     pu.check_final(ids, d, ri, rd, k)
 
 
+def _near_tau(idx, dbg, M, s_max=8192, nnear=8):
+    """The near-list seed's tau where it is exact: the touched lists (nearest
+    probes until >= M vectors) taken whole (<= s_max vectors) -> the M-th
+    smallest dumped est over them; NaN where the seed samples or does not prune."""
+    lo = idx.export()["list_off"]
+    sizes = np.diff(lo)
+    probes = dbg["probes"]
+    ip, est = dbg["scan_ip"], dbg["scan_est"]
+    out = np.full(probes.shape[0], np.nan)
+    off = 0
+    for q in range(probes.shape[0]):
+        blk = [int((sizes[j] + 31) // 32) * 32 for j in probes[q]]
+        cov, npr = 0, 0
+        while npr < min(nnear, len(blk)) and cov < M:
+            cov += int(sizes[probes[q][npr]])
+            npr += 1
+        P = int(sum(sizes[j] for j in probes[q]))
+        if cov >= M and cov <= s_max and P > 2 * M:
+            n = sum(blk[:npr])
+            m = ip[off:off + n] >= 0
+            out[q] = np.sort(est[off:off + n][m])[M - 1]
+        off += sum(blk)
+    return out
+
+
+def _dump_counts(idx, dbg, nprobe, tau):
+    """Per query: the scanned pairs with est <= tau, from the scan dump (pairs in
+    query-major order, ceil(L / 32) 32-slot blocks each, ip = -1 on pad slots)."""
+    lo = idx.export()["list_off"]
+    sizes = np.diff(lo)
+    probes = dbg["probes"]
+    ip, est = dbg["scan_ip"], dbg["scan_est"]
+    out = np.zeros(probes.shape[0], dtype=np.int64)
+    off = 0
+    for q in range(probes.shape[0]):
+        n = int(sum((sizes[j] + 31) // 32 for j in probes[q])) * 32
+        m = ip[off:off + n] >= 0
+        out[q] = int(np.count_nonzero(est[off:off + n][m] <= tau[q]))
+        off += n
+    return out
+
+
 @pytest.mark.parametrize("D,N,nlist,nq", [(128, 40000, 32, 300), (96, 60000, 24, 700), (33, 20000, 16, 200)])
 def test_small_scan_identical(D, N, nlist, nq):
-    """d <= 128: the small-K grouped scan (tiles dealt to 4 epilogue warpgroups,
-    TMEM accumulator ring, dynamic item scheduler) and the generic grouped
-    scan give bit-identical stage outputs: threshold, survivor counts, top-M
-    ids and estimates, every dumped ip / estimate, final ids and distances,
-    with several query groups per list (nq * nprobe / nlist > 256) and ragged
-    Dp (33 -> 64)."""
+    """d <= 128: the folded small-K scan (survivor test on the tensor cores),
+    the small-K scan with the CUDA-core test (VARIANT_NO_FOLD) and the generic
+    grouped scan give bit-identical stage outputs: threshold, top-M ids and
+    estimates, final ids and distances, with several query groups per list
+    (nq * nprobe / nlist > 256) and ragged Dp (33 -> 64).  The two CUDA-core
+    tests flag the same pairs (equal survivor counts); the folded test is
+    conservative: it keeps every pair with est <= tau (counted from the scan
+    dump) and few others.  The uniform-prefix threshold seed
+    (VARIANT_UNIFORM_SEED) changes tau but not the results."""
     X, Q = make_data(D, N, nlist, nq)
     idx = build(X, nlist)
     nprobe = 12 if nlist >= 24 else 8
-    a = debug_search(idx, Q, 10, nprobe, 200, scan_path=rq.SCAN_IMMA)
-    b = debug_search(idx, Q, 10, nprobe, 200, scan_path=rq.SCAN_IMMA, variant=rq.VARIANT_GENERIC_SCAN)
-    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
-    for key in ("tau", "survivors", "topm_ids", "topm_est", "scan_ip", "scan_est"):
-        assert np.array_equal(a[2][key], b[2][key]), key
-    # without the dump (the packed fast survivor test) and with the lower-bound key
+    a = debug_search(idx, Q, 10, nprobe, 200, scan_path=rq.SCAN_IMMA, dump=False)
+    n = debug_search(idx, Q, 10, nprobe, 200, scan_path=rq.SCAN_IMMA, dump=False, variant=rq.VARIANT_NO_FOLD)
+    b = debug_search(idx, Q, 10, nprobe, 200, scan_path=rq.SCAN_IMMA, dump=False, variant=rq.VARIANT_GENERIC_SCAN)
+    for x in (n, b):
+        assert np.array_equal(a[0], x[0]) and np.array_equal(a[1], x[1])
+        for key in ("tau", "topm_ids", "topm_est"):
+            assert np.array_equal(a[2][key], x[2][key]), key
+    assert np.array_equal(n[2]["survivors"], b[2]["survivors"])
+    # the dump runs the CUDA-core test; count the pairs the folded test must keep
+    dmp = debug_search(idx, Q, 10, nprobe, 200, scan_path=rq.SCAN_IMMA)
+    assert np.array_equal(dmp[2]["tau"], a[2]["tau"])
+    # the near-list seed's keys are the scan's: where it takes the touched lists whole,
+    # tau is exactly their M-th smallest est
+    nt = _near_tau(idx, dmp[2], 200)
+    ok = ~np.isnan(nt)
+    assert ok.sum() > 0 and np.array_equal(a[2]["tau"][ok], nt[ok].astype(np.float32))
+    need = _dump_counts(idx, dmp[2], nprobe, a[2]["tau"])
+    assert np.all(a[2]["survivors"] >= need), "folded test dropped a pair with est <= tau"
+    assert a[2]["survivors"].sum() <= need.sum() * 1.01 + 16 * nq
+    u = debug_search(idx, Q, 10, nprobe, 200, scan_path=rq.SCAN_IMMA, dump=False, variant=rq.VARIANT_UNIFORM_SEED)
+    assert np.array_equal(a[0], u[0]) and np.array_equal(a[1], u[1])
+    assert np.array_equal(a[2]["topm_ids"], u[2]["topm_ids"])
+    # without the dump and with the lower-bound key
     for kw in (dict(), dict(rank_key=rq.RANK_LOWER_BOUND)):
         si, sd = idx.search(Q.cuda(), 10, nprobe, 200, scan_path=rq.SCAN_IMMA, **kw)
         gi, gd = idx.search(Q.cuda(), 10, nprobe, 200, scan_path=rq.SCAN_IMMA, variant=rq.VARIANT_GENERIC_SCAN, **kw)
