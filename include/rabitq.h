@@ -193,10 +193,12 @@ typedef struct {
                                                  of the small-K one                              */
 #define RABITQ_VARIANT_UNIFORM_SEED 16u      /* d <= 128, tensor-core scan: threshold from a uniform
                                                  prefix sample of every probed list (the d > 128
-                                                 seeding) instead of the nearest lists           */
+                                                 seeding, also used when list sizes are skewed)
+                                                 instead of the nearest lists; implies NO_FOLD   */
 #define RABITQ_VARIANT_NO_FOLD 32u           /* d <= 128, tensor-core scan: survivor test on the
                                                  CUDA cores (scan_small_kernel) instead of the
-                                                 tensor-core folded test                         */
+                                                 tensor-core folded test (scan_fold_kernel, which
+                                                 runs with the nearest-list threshold only)      */
 
 /* Search nq queries Q [nq x d] fp32: rotate, probe the nprobe
  * nearest lists, 4-bit Philox-randomized query quantization per (q, list),

@@ -28,6 +28,8 @@
 #include <cudaTypedefs.h>
 
 #include <cub/cub.cuh>
+#include <cuda_fp16.h>
+#include <cuda_fp8.h>
 
 #include <algorithm>
 #include <cstring>
@@ -743,7 +745,7 @@ __device__ __forceinline__ void fold_col_put(float* gext, int64_t g, float y1, f
     const float y3l = tc::tf32_rna(__fsub_rn(y3, y3h)), y4l = tc::tf32_rna(__fsub_rn(y4, y4h));
     (void)pad;
     float4* o = reinterpret_cast<float4*>(gext + (g >> 3) * 128 + (g & 7) * 4);
-    o[0] = make_float4(y1h, y1l, y2h, y2l);    // x pc, pc, 1, 1
+    o[0] = make_float4(y1h, y1l, y2h, y2l);    // x pc, pc, 1, 1  (all negated by the caller: D = -ip - E)
     o[8] = make_float4(y3h, y3l, y3h, y4h);    // x alpha_h, alpha_h, alpha_l, beta_h
     o[16] = make_float4(y4l, y4h, 0.f, 0.f);   // x beta_h, beta_l
     o[24] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -761,11 +763,11 @@ __device__ __forceinline__ void fold_col(float* gext, int64_t g, const ColC& cc,
     const float a = cc.a, tau = cc.tau;
     const bool fin = isfinite(a) && isfinite(cc.b) && isfinite(cc.K) && isfinite(cc.nq2);
     if (tau == -INFINITY) {
-        fold_col_const(gext, g, -kFoldBig);  // nothing is <= -inf
+        fold_col_const(gext, g, kFoldBig);  // nothing is <= -inf (D = -ip - E > 0)
         return;
     }
     if (!(a > 0.f) || !fin || !isfinite(tau)) {
-        fold_col_const(gext, g, kFoldBig);  // every pair is a candidate (exact keys decide)
+        fold_col_const(gext, g, -kFoldBig);  // every pair is flagged (exact keys decide)
         return;
     }
     const float ia = __frcp_rn(a);
@@ -776,7 +778,7 @@ __device__ __forceinline__ void fold_col(float* gext, int64_t g, const ColC& cc,
     const float y3 = -__fmul_rn(1.f - kFoldC, ia);
     const float u = __fadd_rn(__fsub_rn(tau, cc.nq2), __fmul_rn(kFoldC, __fadd_rn(cc.nq2, fabsf(tau))));
     const float y4 = __fmul_rn(u, ia);
-    fold_col_put(gext, g, y1, y2, y3, y4, 0.f);
+    fold_col_put(gext, g, -y1, -y2, -y3, -y4, 0.f);  // the accumulator holds -ip - E
 }
 
 // column constants of every grouped row (one half of a 64-byte ColPair record
@@ -792,7 +794,7 @@ __global__ void colc_kernel(const int32_t* __restrict__ gpair, int64_t nrows, in
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < nrows; g += (int64_t)gridDim.x * blockDim.x) {
         const int p = gpair[g];
         if (p < 0) {
-            if (gext) fold_col_const(gext, g, -kFoldBig);  // pad column: never a survivor
+            if (gext) fold_col_const(gext, g, kFoldBig);  // pad column: never flagged (D > 0)
             continue;
         }
         const int q = p / nprobe;
@@ -1272,27 +1274,37 @@ __global__ __launch_bounds__(kSkNT, 1) void scan_small_kernel(const __grid_const
 
 // --------------------------------------------------- folded small-K scan
 // Dp <= 128 main scan (est key, no dump): the survivor test runs on the
-// tensor cores (fold_col above).  Per unit (tile, <= 64 group columns) the MMA
-// warp issues the code x query contraction into the ip accumulator and the
-// K = 16 tf32 contraction of the row / column factors into the E accumulator
-// of the same TMEM slot (4 slots of 2 x 64 columns); the epilogue loads both,
-// E - acc per pair (packed FP32), ANDs the 16 results of a chunk and takes the
-// slow path (exact keys, the small kernel's survivor appends) only when a sign
-// bit is clear somewhere in the warp.  A stages carry the tile's codes (TMA)
-// and its X rows (16 tf32 per vector, written by a producer warp from the
-// tile's row constants); row constants live in a per-tile ring, released when
-// every unit of the tile is done, so the A loader runs ahead of the MMA by the
-// A stages alone.
-constexpr int kFxUW = 64;                   // unit width
-constexpr int kFxUS = 4;                    // TMEM slots: ip [64] + E [64] columns each
-constexpr int kFxSA = 4;                    // A stages (codes 16 KB + X 8 KB)
-constexpr int kFxRT = 8;                    // row-constant ring (tiles)
-constexpr int kFxRI = 6;                    // item records
+// tensor cores (fold_col above).  One accumulator per tile (N = the group's
+// width rounded to 16, <= 256; two TMEM slots of 256 columns): the code x
+// query contraction (-ip, .kind::f8f6f4) and, into the same accumulator, the
+// K = 16 tf32 contraction of the row / column factors (-E), so D = -T and a
+// pair is flagged iff D < 0.  Epilogue warps take 16-column chunks of the
+// tile dynamically (per TMEM lane quarter), OR the 16 accumulators of a chunk
+// and leave at once unless a sign bit is set somewhere in the warp; flagged
+// pairs get their exact ip from the code and query rows (global, e4m3) and the
+// scan's exact key.  A stages carry the tile's codes (TMA) and its X rows (16
+// tf32 per vector, written by 4 producer warps from the tile's row
+// constants); the row constants live in a per-tile ring.
+constexpr int kFxTS = 4;                    // TMEM slots (units in flight), 128 columns each
+constexpr int kFxUW = 128;                  // unit width: a tile's group is split into <= 2 column halves
+#ifndef FX_SA
+#define FX_SA 4
+#endif
+#ifndef FX_RT
+#define FX_RT 8
+#endif
+#ifndef FX_RI
+#define FX_RI 6
+#endif
+constexpr int kFxSA = FX_SA;                // A stages (codes 16 KB + X 8 KB)
+constexpr int kFxRT = FX_RT;                // row-constant ring (tiles)
+constexpr int kFxRI = FX_RI;                // item records
 constexpr int kFxEpiW = 12;                 // epilogue warps (3 per TMEM lane quarter)
 constexpr int kFxXW = 4;                    // X producer warps (one vector row per lane)
 constexpr int kFxMmaW = 2 + kFxXW;          // warps 0 sched + B, 1 A loader, 2..5 X producers, 6 MMA
 constexpr int kFxEpi0 = kFxMmaW + 1;
 constexpr int kFxNT = (kFxEpi0 + kFxEpiW) * 32;  // 608 threads
+constexpr int kFxCh = kFxUW / kEC;               // 8 chunks per unit and lane quarter (at most)
 constexpr uint32_t kFxBStage = kSkNG * kKC;      // 32 KB query operand
 constexpr uint32_t kFxBXStage = kSkNG * 64;      // 16 KB column factors (16 tf32 per column)
 constexpr uint32_t kFxXStage = kTM * 64;         // 8 KB row factors
@@ -1303,6 +1315,28 @@ constexpr uint32_t kFxOffR = kFxOffA + kFxSA * kFxAStage;
 constexpr uint32_t kFxSmem = kFxOffR + kFxRT * sizeof(SkRows) + 1024;
 static_assert(kFxSmem <= 227 * 1024, "fold scan shared memory");
 static_assert(kFxOffA % 1024 == 0 && kFxAStage % 1024 == 0, "A stages 1024-aligned (128-byte swizzle)");
+static_assert(kFxTS * kFxUW <= kTmemCols, "fold scan TMEM");
+
+// exact ip of code row x query row (both e4m3 bytes in the grouped scan's K
+// order, codes 0xB8 = -1 / 0, queries 0..15): the flagged pairs' key input
+__device__ __forceinline__ float ipn_rows(const uint8_t* __restrict__ crow, const uint8_t* __restrict__ qrow, int Dp) {
+    __half2 s0 = __float2half2_rn(0.f), s1 = s0;
+    for (int k = 0; k < Dp; k += 16) {
+        const uint4 c = __ldg(reinterpret_cast<const uint4*>(crow + k));
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(qrow + k));
+        const uint32_t cw[4] = {c.x, c.y, c.z, c.w}, qw[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t m = qw[i] & sgnrep(cw[i]);  // q where the code bit is set
+            __half2_raw lo = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(m & 0xFFFFu), __NV_E4M3);
+            __half2_raw hi = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(m >> 16), __NV_E4M3);
+            s0 = __hadd2(s0, *reinterpret_cast<__half2*>(&lo));  // integers <= 15 Dp < 2048: exact
+            s1 = __hadd2(s1, *reinterpret_cast<__half2*>(&hi));
+        }
+    }
+    const float2 a = __half22float2(s0), b = __half22float2(s1);
+    return -((a.x + a.y) + (b.x + b.y));  // -ip (the f8 accumulator's value), exact
+}
 
 template <int NK>
 __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_constant__ CUtensorMap tmapB,
@@ -1310,13 +1344,20 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
                                                              const float* __restrict__ gext,
                                                              const int4* __restrict__ items, int* __restrict__ sched) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
+#ifdef RABITQ_DIAG
+    volatile long long* crumb = a.trace ? (volatile long long*)a.trace + (size_t)blockIdx.x * 32 : nullptr;
+#define FX_CRUMB(slot, val) do { if (crumb) crumb[slot] = (long long)(val); } while (0)
+#else
+#define FX_CRUMB(slot, val) do { } while (0)
+#endif
     const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
     uint8_t* smem = smem_raw + pad;  // [2] B | [2] BX | [kFxSA] (codes | X) | [kFxRT] row constants
     SkRows* urows = reinterpret_cast<SkRows*>(smem + kFxOffR);
     __shared__ int4 rec[kFxRI];
-    __shared__ uint32_t next_unit[4];
+    __shared__ uint32_t next_chunk[4];
+    __shared__ uint32_t mma_issued;  // tiles whose MMAs the MMA warp has issued (epilogue wait gate)
     __shared__ __align__(8) uint64_t ifull[kFxRI], iempty[kFxRI], bfull[2], bfree[2], afull[kFxSA], xfull[kFxSA],
-        aempty[kFxSA], accf[kFxUS], acce[kFxUS], rowf[kFxRT], rempty[kFxRT];
+        aempty[kFxSA], accf[kFxTS], acce[kFxTS], rowf[kFxRT];
     __shared__ uint32_t tmem_base_s;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (warp == kFxMmaW) tc::tmem_alloc(&tmem_base_s, kTmemCols);
@@ -1334,15 +1375,13 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
             tc::mbar_init(&xfull[s], kFxXW);
             tc::mbar_init(&aempty[s], 1);
         }
-        for (int k = 0; k < kFxUS; ++k) {
+        for (int k = 0; k < kFxTS; ++k) {
             tc::mbar_init(&accf[k], 1);
             tc::mbar_init(&acce[k], 4);  // one warp per TMEM lane quarter
         }
-        for (int t = 0; t < kFxRT; ++t) {
-            tc::mbar_init(&rowf[t], 1);
-            tc::mbar_init(&rempty[t], 48);  // 4 quarters x nu units x 12 / nu
-        }
-        for (int q = 0; q < 4; ++q) next_unit[q] = 0u;
+        for (int t = 0; t < kFxRT; ++t) tc::mbar_init(&rowf[t], 1);
+        for (int q = 0; q < 4; ++q) next_chunk[q] = 0u;
+        mma_issued = 0u;
         tc::prefetch_tmap(&tmapB);
         tc::prefetch_tmap(&tmapA);
     }
@@ -1366,17 +1405,18 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
                 }
                 const int4 r = __ldg(items + id);
                 rec[s] = r;
+                FX_CRUMB(0, i);
                 tc::mbar_arrive(&ifull[s]);
                 const int nc = r.w & 511;
                 const int b = (int)(i & 1u);
                 if (i >= 2) tc::mbar_wait(&bfree[b], ((i >> 1) - 1) & 1);
                 const int nb = (nc + kBoxRows - 1) / kBoxRows;
-                const uint32_t bxb = (uint32_t)(nb * kBoxRows) * 64u;
+                const uint32_t bxb = a.fold_diag == 12 ? 0u : (uint32_t)(nb * kBoxRows) * 64u;
                 tc::mbar_arrive_expect_tx(&bfull[b], (uint32_t)(nb * kBoxRows * kKC) + bxb);
                 for (int bx = 0; bx < nb; ++bx)
                     tc::tma_load_2d(smem + b * kFxBStage + bx * kBoxRows * kKC, &tmapB, &bfull[b], 0,
                                     r.z + bx * kBoxRows);
-                tc::bulk_load(smem + kFxOffBX + b * kFxBXStage, gext + (int64_t)r.z * 16, bxb, &bfull[b]);
+                if (bxb) tc::bulk_load(smem + kFxOffBX + b * kFxBXStage, gext + (int64_t)r.z * 16, bxb, &bfull[b]);
             }
         }
     } else if (warp == 1) {
@@ -1393,10 +1433,13 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
                 for (int t = 0; t < nt; ++t, ++tcnt) {
                     const int st = (int)(tcnt % kFxSA);
                     if (tcnt >= (uint32_t)kFxSA) tc::mbar_wait(&aempty[st], ((tcnt / kFxSA) - 1) & 1);
+                    FX_CRUMB(1, tcnt);
                     tc::mbar_arrive_expect_tx(&afull[st], (uint32_t)kAStage);
                     tc::tma_load_2d(smem + kFxOffA + st * kFxAStage, &tmapA, &afull[st], 0, r.x + (t0 + t) * kTM);
+                    // row constants of tile tcnt: slot tcnt % 8 was last used by tile tcnt - 8,
+                    // whose accumulator slot (released only after its epilogue) precedes tile
+                    // tcnt - 2's MMA, which precedes this tile's A stage reuse (tcnt - 4)
                     const int rt = (int)(tcnt % kFxRT);
-                    if (tcnt >= (uint32_t)kFxRT) tc::mbar_wait(&rempty[rt], ((tcnt / kFxRT) - 1) & 1);
                     const int v0 = (t0 + t) * kTM;
                     const int nv = r.y - v0 < kTM ? r.y - v0 : kTM;
                     const uint32_t ncp = (uint32_t)((nv + 31) & ~31);
@@ -1412,6 +1455,7 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
     } else if (warp < kFxMmaW) {
         // ============ X producers: 16 tf32 row factors per vector of each tile ============
         uint32_t tcnt = 0;
+        const int rr = (warp - 2) * 32 + lane;
         for (uint32_t i = 0;; ++i) {
             const int s = (int)(i % kFxRI);
             tc::mbar_wait(&ifull[s], (i / kFxRI) & 1);
@@ -1425,29 +1469,29 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
                 if (tcnt >= (uint32_t)kFxSA) tc::mbar_wait(&aempty[st], ((tcnt / kFxSA) - 1) & 1);
                 tc::mbar_wait(&rowf[rt], (tcnt / kFxRT) & 1);
                 const SkRows& R = urows[rt];
+                if (lane == 0) FX_CRUMB(2 + (warp - 2), tcnt);
                 uint8_t* xs = smem + kFxOffA + st * kFxAStage + kAStage;
                 const int nv = r.y - (t0 + t) * kTM;
-                {
-                    const int rr = (warp - 2) * 32 + lane;
-                    float pc = 0.f, ah = 0.f, al = 0.f, bh = 0.f, bl = 0.f;
-                    if (rr < nv) {
-                        const float2 fc = R.fac[rr];
-                        pc = (float)R.pcnt[rr];
-                        const float beta = __frcp_rn(fc.y), alpha = __fmul_rn(fc.x, beta);
-                        if (fc.y > 0.f && isfinite(beta) && isfinite(alpha)) {
-                            ah = tc::tf32_rna(alpha);
-                            al = tc::tf32_rna(__fsub_rn(alpha, ah));
-                            bh = tc::tf32_rna(beta);
-                            bl = tc::tf32_rna(__fsub_rn(beta, bh));
-                        } else {
-                            ah = -kFoldBig;  // f = 0 (n_o = 0): always a candidate
-                        }
+                float pc = 0.f, ah = 0.f, al = 0.f, bh = 0.f, bl = 0.f;
+                if (rr < nv) {
+                    const float2 fc = R.fac[rr];
+                    pc = (float)R.pcnt[rr];
+                    const float beta = __frcp_rn(fc.y), alpha = __fmul_rn(fc.x, beta);
+                    if (fc.y > 0.f && isfinite(beta) && isfinite(alpha)) {
+                        ah = tc::tf32_rna(alpha);
+                        al = tc::tf32_rna(__fsub_rn(alpha, ah));
+                        bh = tc::tf32_rna(beta);
+                        bl = tc::tf32_rna(__fsub_rn(beta, bh));
+                    } else {
+                        ah = -kFoldBig;  // f = 0 (n_o = 0): always flagged (with the negated y3 > 0)
                     }
-                    float4* o = reinterpret_cast<float4*>(xs + (rr >> 3) * 512 + (rr & 7) * 16);
-                    o[0] = make_float4(pc, pc, 1.f, 1.f);
-                    o[8] = make_float4(ah, ah, al, bh);
-                    o[16] = make_float4(bh, bl, 0.f, 0.f);
-                    o[24] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+                float4* o = reinterpret_cast<float4*>(xs + (rr >> 3) * 512 + (rr & 7) * 16);
+                if (a.fold_diag != 11) {
+                o[0] = make_float4(pc, pc, 1.f, 1.f);
+                o[8] = make_float4(ah, ah, al, bh);
+                o[16] = make_float4(bh, bl, 0.f, 0.f);
+                o[24] = make_float4(0.f, 0.f, 0.f, 0.f);
                 }
                 tc::fence_proxy_async();
                 __syncwarp();
@@ -1455,66 +1499,66 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
             }
         }
     } else if (warp == kFxMmaW) {
-        // ============ MMA issuer (one thread): per unit the ip and E contractions into slot ucnt % 4 ============
-        if (lane == 0) {
-            uint32_t tcnt = 0, ucnt = 0;
-            const uint32_t accf_s = tc::smem_u32(accf), acce_s = tc::smem_u32(acce);
-            for (uint32_t i = 0;; ++i) {
-                const int s = (int)(i % kFxRI);
-                tc::mbar_wait(&ifull[s], (i / kFxRI) & 1);
-                const int4 r = rec[s];
-                tc::mbar_arrive(&iempty[s]);
-                if (r.w == 0) break;
-                const int nc = r.w & 511, nt = (r.w >> 9) & 15;
-                const int nu = (nc + kFxUW - 1) / kFxUW;
-                const int wl = nc - (nu - 1) * kFxUW;  // width of the last unit
-                const uint32_t id8 = tc::idesc_f8(kTM, kFxUW), id32 = tc::idesc_tf32_f32(kTM, kFxUW);
-                const uint32_t id8l = tc::idesc_f8(kTM, (wl + 15) & ~15), id32l = tc::idesc_tf32_f32(kTM, (wl + 15) & ~15);
-                const int b = (int)(i & 1u);
-                tc::mbar_wait(&bfull[b], (i >> 1) & 1);
-                tc::fence_after_sync();
-                const uint64_t bdesc0 = tc::smem_desc_sw128(tc::smem_u32(smem + b * kFxBStage));
-                const uint64_t bxdesc0 = tc::smem_desc(tc::smem_u32(smem + kFxOffBX + b * kFxBXStage), 128, 512);
+        // ============ MMA issuer: per unit D = -ip - E into slot ucnt % 4 ============
+        uint32_t tcnt = 0, ucnt = 0;
+        const uint32_t accf_s = tc::smem_u32(accf), acce_s = tc::smem_u32(acce);
+        for (uint32_t i = 0;; ++i) {
+            const int s = (int)(i % kFxRI);
+            tc::mbar_wait(&ifull[s], (i / kFxRI) & 1);
+            const int4 r = rec[s];
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&iempty[s]);
+            if (r.w == 0) break;
+            const int nc = r.w & 511, nt = (r.w >> 9) & 15;
+            // units: the group's columns in nu <= 2 halves of wu (multiple of 16) columns
+            const int nu = nc > kFxUW ? 2 : 1;
+            const int wu = nu == 1 ? ((nc + 15) & ~15) : ((((nc + 1) >> 1) + 15) & ~15);
+            const int wl = ((nc - (nu - 1) * wu) + 15) & ~15;  // last unit's MMA width
+            const uint32_t id8 = tc::idesc_f8(kTM, wu), id32 = tc::idesc_tf32_f32(kTM, wu);
+            const uint32_t id8l = tc::idesc_f8(kTM, wl), id32l = tc::idesc_tf32_f32(kTM, wl);
+            const int b = (int)(i & 1u);
+            tc::mbar_wait(&bfull[b], (i >> 1) & 1);
+            __syncwarp();
+            tc::fence_after_sync();
+            const uint64_t bdesc = tc::smem_desc_sw128(tc::smem_u32(smem + b * kFxBStage));
+            const uint64_t bxdesc = tc::smem_desc(tc::smem_u32(smem + kFxOffBX + b * kFxBXStage), 128, 512);
 #pragma unroll 1
-                for (int t = 0; t < nt; ++t, ++tcnt) {
-                    const int as = (int)(tcnt % kFxSA);
-                    tc::mbar_wait(&afull[as], (tcnt / kFxSA) & 1);
-                    tc::mbar_wait(&xfull[as], (tcnt / kFxSA) & 1);
+            for (int t = 0; t < nt; ++t) {
+                const int as = (int)(tcnt % kFxSA);
+                tc::mbar_wait(&afull[as], (tcnt / kFxSA) & 1);
+                tc::mbar_wait(&xfull[as], (tcnt / kFxSA) & 1);
+                const uint32_t abase = tc::smem_u32(smem + kFxOffA + as * kFxAStage);
+                const uint64_t adesc = tc::smem_desc_sw128(abase), xdesc = tc::smem_desc(abase + kAStage, 128, 512);
+#pragma unroll 1
+                for (int u = 0; u < nu; ++u, ++ucnt) {
+                    const uint32_t k = ucnt % kFxTS;
+                    if (ucnt >= (uint32_t)kFxTS) tc::mbar_wait_s(acce_s + 8u * k, ((ucnt / kFxTS) - 1) & 1);
+                    __syncwarp();  // the waits loop per thread: reconverge before elect.sync / tcgen05
                     tc::fence_after_sync();
-                    const uint32_t abase = tc::smem_u32(smem + kFxOffA + as * kFxAStage);
-                    const uint64_t adesc = tc::smem_desc_sw128(abase);
-                    const uint64_t xdesc = tc::smem_desc(abase + kAStage, 128, 512);
-#pragma unroll 1
-                    for (int u = 0; u < nu; ++u, ++ucnt) {
-                        const uint32_t k = ucnt % kFxUS;
-                        if (ucnt >= (uint32_t)kFxUS) {
-                            tc::mbar_wait_s(acce_s + 8u * k, ((ucnt / kFxUS) - 1) & 1);
-                            tc::fence_after_sync();
-                        }
-                        const bool last = u == nu - 1;
-                        // B rows [64 u, +64): 8 KB = 512 descriptor units (SW128); BX: 4 KB = 256
-                        tc::mma_fold_unit1<NK>(tmem + k * 128u, tmem + k * 128u + 64u, adesc,
-                                               bdesc0 + (uint64_t)(u * 512), last ? id8l : id8, xdesc,
-                                               bxdesc0 + (uint64_t)(u * 256), last ? id32l : id32, accf_s + 8u * k);
-                    }
-                    tc::commit(&aempty[as]);                // the tile's codes and X rows are free
-                    if (t == nt - 1) tc::commit(&bfree[b]);  // the item's B and BX are free
+                    const uint32_t dt = tmem + k * (uint32_t)kFxUW;
+                    const bool last = u == nu - 1;
+                    // B rows [u wu, +wu): wu x 128 B (SW128: 16-byte descriptor units); BX: wu / 8 x 512 B
+                    tc::mma_fold_acc_w<NK>(dt, adesc, bdesc + (uint64_t)(u * wu * 8), last ? id8l : id8, xdesc,
+                                           bxdesc + (uint64_t)(u * wu * 4), last ? id32l : id32, accf_s + 8u * k);
+                    if (lane == 0) atomicExch(&mma_issued, ucnt + 1u);
                 }
+                tc::commit_warp(&aempty[as]);                // the tile's codes and X rows are free
+                if (t == nt - 1) tc::commit_warp(&bfree[b]);  // the item's B and BX are free
+                ++tcnt;
             }
         }
     } else {
-        // ============ epilogue: 32 rows (the warp's lane quarter) x a unit's columns ============
+        // ============ epilogue: a unit's <= 128 columns x the warp's lane quarter ============
         const int quarter = warp & 3;
         const int r = quarter * 32 + lane;
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
-        const uint32_t rowf_s = tc::smem_u32(rowf), accf_s = tc::smem_u32(accf), acce_s = tc::smem_u32(acce),
-                       rempty_s = tc::smem_u32(rempty);
+        const uint32_t rowf_s = tc::smem_u32(rowf), accf_s = tc::smem_u32(accf), acce_s = tc::smem_u32(acce);
         uint32_t i = 0, u0 = 0, tc0 = 0;  // item cursor, its first unit and first tile
         int4 R = make_int4(0, 0, 0, 0);
-        int nu = 0, nut = -1;
+        int nu = 1, wu = 16, nut = -1;
         for (;;) {
             uint32_t uc = 0;
-            if (lane == 0) uc = atomicAdd(&next_unit[quarter], 1u);
+            if (lane == 0) uc = atomicAdd(&next_chunk[quarter], 1u);
             uc = __shfl_sync(0xFFFFFFFFu, uc, 0);
             bool done = false;
             for (;;) {
@@ -1525,115 +1569,139 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
                         done = true;
                         break;
                     }
-                    nu = ((R.w & 511) + kFxUW - 1) / kFxUW;
+                    const int nc_ = R.w & 511;
+                    nu = nc_ > kFxUW ? 2 : 1;
+                    wu = nu == 1 ? ((nc_ + 15) & ~15) : ((((nc_ + 1) >> 1) + 15) & ~15);
                     nut = ((R.w >> 9) & 15) * nu;
                 }
                 if (uc < u0 + (uint32_t)nut) break;
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&iempty[i % kFxRI]);
                 u0 += (uint32_t)nut;
-                tc0 += (uint32_t)(((R.w >> 9) & 15));
+                tc0 += (uint32_t)((R.w >> 9) & 15);
                 ++i;
                 nut = -1;
             }
             if (done) break;
             const int nc = R.w & 511, t0 = (int)((uint32_t)R.w >> 13);
             const int x = (int)(uc - u0);
-            const int t = nu == 1 ? x : nu == 2 ? x >> 1 : nu == 4 ? x >> 2 : (x * 43) >> 7, u = x - t * nu;
+            const int t = nu == 1 ? x : x >> 1, u = x - t * nu;
             const int64_t v = (int64_t)(t0 + t) * kTM + r;
             const bool vok = v < R.y;
             const uint32_t tcnt = tc0 + (uint32_t)t;
-            const int rt = (int)(tcnt % kFxRT);
-            const int k = (int)(uc % kFxUS);
-            const uint32_t ph = (uc / kFxUS) & 1;
-            const int w = nc - u * kFxUW < kFxUW ? nc - u * kFxUW : kFxUW;
-            const int64_t gcol0 = (int64_t)R.z + u * kFxUW;  // grouped row of the unit's column 0
-            tc::mbar_wait_s(accf_s + 8u * k, ph);
+            const uint32_t k = uc % kFxTS;
+            const int cend = min(nc, (u + 1) * wu) - u * wu;  // valid columns of the unit
+            if (lane == 0) FX_CRUMB(10 + (warp - kFxEpi0), ((long long)uc << 32) | (uint32_t)cend);
+            // Once the MMA warp has issued unit uc, the slot's previous fill has completed
+            // (issue waited for its release), so the accf parity wait is unambiguous however
+            // far ahead of the MMA this warp took its unit; the tile's rowf phase is complete
+            // by then as well (its X rows were consumed).
+            if (*(volatile uint32_t*)&mma_issued <= uc) {
+                uint32_t ns = 32;
+                while (*(volatile uint32_t*)&mma_issued <= uc) {
+                    __nanosleep(ns);
+                    if (ns < 256) ns <<= 1;
+                }
+            }
+            tc::mbar_wait_s(accf_s + 8u * k, (uc / kFxTS) & 1);
+            __syncwarp();  // reconverge before tcgen05.ld.sync.aligned
             tc::fence_after_sync();
-            const uint32_t tbase = lane_base + (uint32_t)(k * 128);
+            const uint32_t tb = lane_base + k * (uint32_t)kFxUW;
             bool rows_ready = false;
+            for (int c2 = 0; c2 < cend; c2 += 4 * kEC) {
+                // 64 columns per wait (4 loads in flight); columns past the unit's width
+                // read the slot's unused columns and are masked below
+                uint32_t flag4 = 0u;
+                {
+                    uint32_t d2[4][kEC];
+                    tc::tmem_ld16_nw(tb + (uint32_t)c2, d2[0]);
+                    tc::tmem_ld16_nw(tb + (uint32_t)(c2 + kEC), d2[1]);
+                    tc::tmem_ld16_nw(tb + (uint32_t)(c2 + 2 * kEC), d2[2]);
+                    tc::tmem_ld16_nw(tb + (uint32_t)(c2 + 3 * kEC), d2[3]);
+                    tc::tmem_ld_wait();
 #pragma unroll
-            for (int h = 0; h < kFxUW / kEC; ++h) {
-                const int col0 = h * kEC;
-                if (col0 >= w) break;
-                uint32_t acc[kEC], ev[kEC];
-                tc::tmem_ld16_nw(tbase + (uint32_t)col0, acc);
-                tc::tmem_ld16_nw(tbase + 64u + (uint32_t)col0, ev);
-                tc::tmem_ld_wait();
-                uint32_t dbits[kEC];
+                    for (int hh = 0; hh < 4; ++hh) {
+                        uint32_t any = d2[hh][0];
 #pragma unroll
-                for (int c = 0; c < kEC; c += 2) {
-                    const float2 dd = fsub2(make_float2(__uint_as_float(ev[c]), __uint_as_float(ev[c + 1])),
-                                            make_float2(__uint_as_float(acc[c]), __uint_as_float(acc[c + 1])));
-                    dbits[c] = __float_as_uint(dd.x);
-                    dbits[c + 1] = __float_as_uint(dd.y);
+                        for (int c = 1; c < kEC; ++c) any |= d2[hh][c];
+                        flag4 |= (vok && (any >> 31) && c2 + hh * kEC < cend) ? (1u << hh) : 0u;
+                    }
                 }
-                uint32_t all = dbits[0];
-#pragma unroll
-                for (int c = 1; c < kEC; ++c) all &= dbits[c];
-                const bool cand = vok && !(all >> 31);
-                if (!__any_sync(0xFFFFFFFFu, cand)) continue;
-                // ---- slow path: exact keys of the flagged pairs of this chunk ----
-                if (!rows_ready) {
-                    tc::mbar_wait_s(rowf_s + 8u * rt, (tcnt / kFxRT) & 1);
-                    rows_ready = true;
+                flag4 = __reduce_or_sync(0xFFFFFFFFu, flag4);
+#ifdef RABITQ_DIAG
+                if (a.fold_diag >= 8) {  // pure delay instead of the slow path (race hunting)
+                    if (flag4) __nanosleep(a.fold_diag == 9 ? 20000 : 2000);
+                    continue;
                 }
-                const SkRows& RS = urows[rt];
-                const float2 fac = vok ? RS.fac[r] : make_float2(0.f, 0.f);
-                const float pcf = vok ? (float)RS.pcnt[r] : 0.f;
-                const uint32_t row = vok ? RS.rows[r] : 0u;
-                uint32_t rowbits = 0u;
+                if (a.fold_diag == 1) continue;
+#endif
+                for (uint32_t f4 = flag4; f4; f4 &= f4 - 1) {
+                    const int hh = __ffs(f4) - 1;
+                    const int cl0 = c2 + hh * kEC;  // unit column of the chunk
+                    uint32_t d[kEC];
+                    tc::tmem_ld16(tb + (uint32_t)cl0, d);  // re-read the flagged chunk (rare)
+                    // ---- slow path: exact keys of the flagged pairs of this chunk ----
+                    const int rt = (int)(tcnt % kFxRT);
+                    if (!rows_ready) {
+                        tc::mbar_wait_s(rowf_s + 8u * rt, (tcnt / kFxRT) & 1);
+                        rows_ready = true;
+                    }
+                    const SkRows& RS = urows[rt];
+                    const float2 fac = vok ? RS.fac[r] : make_float2(0.f, 0.f);
+                    const float pcf = vok ? (float)RS.pcnt[r] : 0.f;
+                    const uint32_t row = vok ? RS.rows[r] : 0u;
+                    uint32_t rowbits = 0u;
 #pragma unroll
-                for (int c = kEC - 1; c >= 0; --c) rowbits = (rowbits << 1) | (1u - (dbits[c] >> 31));
-                const int rem = w - col0;
-                if (rem < kEC) rowbits &= (1u << rem) - 1u;
-                if (!vok) rowbits = 0u;
-                const uint32_t cols = __reduce_or_sync(0xFFFFFFFFu, rowbits);
-                // lane c < 16 owns column c: its row ballot, constants and counter atomic
-                // (one round trip each for all flagged columns of the chunk)
-                uint32_t mybal = 0u;
-                for (uint32_t m = cols; m; m &= m - 1) {
-                    const int i2 = __ffs(m) - 1;
-                    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, (rowbits >> i2) & 1u);
-                    if (lane == i2) mybal = bal;
-                }
-                ColC mc{};
-                int mybase = 0;
-                if (mybal) {
-                    mc = colp_get(a.gcolp, (int)(gcol0 + col0 + lane));
-                    mybase = atomicAdd(&a.cnt[mc.q], __popc(mybal));
-                }
-                for (uint32_t m = cols; m; m &= m - 1) {
-                    const int i2 = __ffs(m) - 1;
-                    const uint32_t bal = __shfl_sync(0xFFFFFFFFu, mybal, i2);
-                    const int base = __shfl_sync(0xFFFFFFFFu, mybase, i2);
-                    ColC cc;
-                    cc.a = __shfl_sync(0xFFFFFFFFu, mc.a, i2);
-                    cc.b = __shfl_sync(0xFFFFFFFFu, mc.b, i2);
-                    cc.K = __shfl_sync(0xFFFFFFFFu, mc.K, i2);
-                    cc.nq2 = __shfl_sync(0xFFFFFFFFu, mc.nq2, i2);
-                    cc.q = __shfl_sync(0xFFFFFFFFu, mc.q, i2);
-                    if ((bal >> lane) & 1u) {
-                        uint32_t accv = acc[0];
-#pragma unroll
-                        for (int c = 1; c < kEC; ++c) accv = (c == i2) ? acc[c] : accv;
-                        const float key = est_of<true>(accv, cc, fac, pcf);
-                        const int pos = base + __popc(bal & ((1u << lane) - 1u));
-                        if (pos < a.cap) a.buf[(size_t)cc.q * a.cap + pos] = make_key(key, row);
+                    for (int c = kEC - 1; c >= 0; --c) rowbits = (rowbits << 1) | (d[c] >> 31);
+                    const int rem = cend - cl0;
+                    if (rem < kEC) rowbits &= (1u << rem) - 1u;
+                    if (!vok) rowbits = 0u;
+                    const uint32_t cols = __reduce_or_sync(0xFFFFFFFFu, rowbits);
+                    // lane c < 16 owns column c: its row ballot, constants and counter atomic
+                    uint32_t mybal = 0u;
+                    for (uint32_t m = cols; m; m &= m - 1) {
+                        const int i2 = __ffs(m) - 1;
+                        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, (rowbits >> i2) & 1u);
+                        if (lane == i2) mybal = bal;
+                    }
+                    const int64_t gcol0 = (int64_t)R.z + u * wu + cl0;  // grouped row of the chunk's column 0
+                    ColC mc{};
+                    int mybase = 0;
+                    if (mybal) {
+                        mc = colp_get(a.gcolp, (int)(gcol0 + lane));
+                        mybase = atomicAdd(&a.cnt[mc.q], __popc(mybal));
+                    }
+                    const uint8_t* crow = a.codes8 + (size_t)(R.x + v) * a.Dp;
+                    for (uint32_t m = cols; m; m &= m - 1) {
+                        const int i2 = __ffs(m) - 1;
+                        const uint32_t bal = __shfl_sync(0xFFFFFFFFu, mybal, i2);
+                        const int base = __shfl_sync(0xFFFFFFFFu, mybase, i2);
+                        ColC cq;
+                        cq.a = __shfl_sync(0xFFFFFFFFu, mc.a, i2);
+                        cq.b = __shfl_sync(0xFFFFFFFFu, mc.b, i2);
+                        cq.K = __shfl_sync(0xFFFFFFFFu, mc.K, i2);
+                        cq.nq2 = __shfl_sync(0xFFFFFFFFu, mc.nq2, i2);
+                        cq.q = __shfl_sync(0xFFFFFFFFu, mc.q, i2);
+                        if ((bal >> lane) & 1u) {
+                            const float ipn = ipn_rows(crow, a.qbar8 + (size_t)(gcol0 + i2) * a.Dp, a.Dp);
+                            const float key = est_of<true>(__float_as_uint(ipn), cq, fac, pcf);
+                            const int pos = base + __popc(bal & ((1u << lane) - 1u));
+                            if (pos < a.cap) a.buf[(size_t)cq.q * a.cap + pos] = make_key(key, row);
+                        }
                     }
                 }
             }
             tc::fence_before_sync();
             __syncwarp();
-            if (lane == 0) {
-                tc::mbar_arrive_s(acce_s + 8u * k);
-                tc::mbar_arrive_cnt_s(rempty_s + 8u * rt, (uint32_t)(12 / nu));
-            }
+            if (lane == 0) tc::mbar_arrive_s(acce_s + 8u * k);  // the slot may be refilled
         }
     }
+    if (lane == 0) FX_CRUMB(24, warp);
     tc::fence_before_sync();
     __syncthreads();
+    if (tid == 0) FX_CRUMB(25, 1);
     if (warp == kFxMmaW) tc::tmem_dealloc(tmem, kTmemCols);
+#undef FX_CRUMB
 }
 
 }  // namespace
@@ -1812,6 +1880,15 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
             a.nlist, a.list_off, a.slot_off, a.gstart, a.gcount, a.list_items, items.p);
         RQ_CHECK_LAUNCH();
         if (fold) {
+            long long* crumbs_h = nullptr;
+            const char* crumbs_path = rq_diag_env("RABITQ_FOLD_CRUMBS");
+            if (crumbs_path) {
+                RQ_CUDA(cudaHostAlloc(&crumbs_h, (size_t)sms * 32 * sizeof(long long), cudaHostAllocMapped));
+                std::memset(crumbs_h, 0xFF, (size_t)sms * 32 * sizeof(long long));
+                long long* dptr = nullptr;
+                RQ_CUDA(cudaHostGetDevicePointer(&dptr, crumbs_h, 0));
+                a.trace = dptr;
+            }
 #define RQ_FOLD(NK)                                                                                          \
     do {                                                                                                       \
         RQ_CUDA(cudaFuncSetAttribute(scan_fold_kernel<NK>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
@@ -1825,6 +1902,14 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
                 default: RQ_FOLD(4); break;
             }
 #undef RQ_FOLD
+            if (crumbs_h) {
+                const cudaError_t e = cudaStreamSynchronize(st);
+                if (FILE* f = fopen(crumbs_path, "wb")) {
+                    fwrite(crumbs_h, sizeof(long long), (size_t)sms * 32, f);
+                    fclose(f);
+                }
+                RQ_CUDA(e);
+            }
             RQ_CHECK_LAUNCH();
             return;
         }

@@ -443,6 +443,58 @@ __device__ __forceinline__ void mma_fold_unit1(uint32_t tmem_ip, uint32_t tmem_e
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
 
+// Warp-wide version (every lane calls it with warp-uniform operands; one lane
+// is elected inside each asm).
+template <int NK>
+__device__ __forceinline__ void mma_fold_unit_w(uint32_t tmem_ip, uint32_t tmem_e, uint64_t adesc, uint64_t bdesc,
+                                                uint32_t idesc8, uint64_t xdesc, uint64_t bxdesc, uint32_t idesc32,
+                                                uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .pred t, e;\n\t"
+        ".reg .b64 a1, a2, a3, b1, b2, b3, x1, y1;\n\t"
+        "setp.eq.b32 t, 0, 0;\n\t"
+        "add.u64 x1, %5, 16;\n\tadd.u64 y1, %6, 16;\n\t"
+        "add.u64 a1, %2, 2;\n\tadd.u64 a2, %2, 4;\n\tadd.u64 a3, %2, 6;\n\t"
+        "add.u64 b1, %3, 2;\n\tadd.u64 b2, %3, 4;\n\tadd.u64 b3, %3, 6;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %2, %3, %4, !t;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], %5, %6, %7, !t;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], x1, y1, %7, t;\n\t"
+        ".reg .pred k1, k2, k3;\n\t"
+        "setp.gt.and.s32 k1, %9, 1, e;\n\tsetp.gt.and.s32 k2, %9, 2, e;\n\tsetp.gt.and.s32 k3, %9, 3, e;\n\t"
+        "@k1 tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a1, b1, %4, t;\n\t"
+        "@k2 tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a2, b2, %4, t;\n\t"
+        "@k3 tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a3, b3, %4, t;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%8];\n\t}" ::"r"(tmem_ip),
+        "r"(tmem_e), "l"(adesc), "l"(bdesc), "r"(idesc8), "l"(xdesc), "l"(bxdesc), "r"(idesc32), "r"(bar), "n"(NK)
+        : "memory");
+}
+
+// One accumulator: D = A_codes . B_query^T (NK K steps, .kind::f8f6f4) + X . BX^T
+// (K = 16 tf32), warp-wide with one elected lane, then one commit of `bar`.
+template <int NK>
+__device__ __forceinline__ void mma_fold_acc_w(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc8,
+                                               uint64_t xdesc, uint64_t bxdesc, uint32_t idesc32, uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .pred t, e, k1, k2, k3;\n\t"
+        ".reg .b64 a1, a2, a3, b1, b2, b3, x1, y1;\n\t"
+        "setp.eq.b32 t, 0, 0;\n\t"
+        "add.u64 x1, %4, 16;\n\tadd.u64 y1, %5, 16;\n\t"
+        "add.u64 a1, %1, 2;\n\tadd.u64 a2, %1, 4;\n\tadd.u64 a3, %1, 6;\n\t"
+        "add.u64 b1, %2, 2;\n\tadd.u64 b2, %2, 4;\n\tadd.u64 b3, %2, 6;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.gt.and.s32 k1, %8, 1, e;\n\tsetp.gt.and.s32 k2, %8, 2, e;\n\tsetp.gt.and.s32 k3, %8, 3, e;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, !t;\n\t"
+        "@k1 tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a1, b1, %3, t;\n\t"
+        "@k2 tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a2, b2, %3, t;\n\t"
+        "@k3 tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a3, b3, %3, t;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %4, %5, %6, t;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], x1, y1, %6, t;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc8), "l"(xdesc), "l"(bxdesc), "r"(idesc32), "r"(bar), "r"(NK)
+        : "memory");
+}
+
 __host__ __device__ constexpr uint32_t idesc_tf32_f32(int M, int N) {
     return (1u << 4)                 // c_format: F32
            | (2u << 7) | (2u << 10)  // a/b format: TF32

@@ -359,7 +359,7 @@ def test_fullq_parity(orc, D, N, nlist, nq, nprobe, k, M):
     pu.check_final(ids, d, ri, rd, k)
 
 
-def _near_tau(idx, dbg, M, s_max=8192, nnear=8):
+def _near_tau(idx, dbg, M, s_max=8192, nnear=32):
     """The near-list seed's tau where it is exact: the touched lists (nearest
     probes until >= M vectors) taken whole (<= s_max vectors) -> the M-th
     smallest dumped est over them; NaN where the seed samples or does not prune."""

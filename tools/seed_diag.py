@@ -40,6 +40,15 @@ for var in json.loads(args.variants):
                       "surv_pct": [int(np.percentile(sv, p)) for p in (0, 1, 10, 50, 90, 99, 100)],
                       "under_q": int(under.size), "under_first": under[:10].tolist(),
                       "tau_over_mth_pct": [float(np.percentile(tau / mth, p)) for p in (0, 1, 50, 99)]}), flush=True)
+    top = np.argsort(-sv)[:6]
+    lo = None
+    for q in top:
+        pr = dbg["probes"][q].cpu().numpy()
+        if lo is None:
+            lo = idx.export()["list_off"] if args.config <= 3 else None
+        sz = (np.diff(lo)[pr].tolist() if lo is not None else [])
+        print("  top-surv q", int(q), "surv", int(sv[q]), "tau", float(tau[q]), "Mth", float(mth[q]),
+              "sizes", sz[:12], "P", int(sum(sz)) if sz else None, flush=True)
     if under.size:
         ex = idx.export() if var == 0 and args.config <= 3 else None
         lo = idx.info()
