@@ -343,7 +343,7 @@ def run_ours(args):
     surv = float(np.mean([p["survivors"] for p in profs]))
     max_surv = int(max(p["max_survivors"] for p in profs))
     retries = int(max(p["retries"] for p in profs))
-    imma = profs[0]["scan_path_used"] == 2
+    imma = profs[0]["scan_path_used"] in (2, 3)
     launches = int(round(np.mean([p["kernel_launches"] for p in profs])))
     W = s.W
     scan_bytes = pairs * (4 * W + 8)  # code words + {n_o^2, f1} per (query, vector) pair
@@ -377,7 +377,7 @@ def run_ours(args):
                 "peak": round(alu_peak, 2), "algorithmic": alu_ops,
                 "peak_source": "148 SMs x 128 FP32 lanes x sm_max_mhz (MEASURED_PEAKS.json), 1 op per lane-instruction"}
     small_k = imma and s.D <= 128
-    fold = small_k and not (args.variant & (32 | 8))  # VARIANT_NO_FOLD / GENERIC_SCAN: the CUDA-core test
+    fold = small_k and profs[0]["scan_path_used"] == 3  # the folded tensor-core survivor test ran
     if fold:
         # folded small-K scan: the survivor test runs on the tensor cores, so
         # the tensor pipe is the roof.  Algorithmic work = the e4m3 ip contraction, 2 D ops per

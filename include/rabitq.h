@@ -129,7 +129,8 @@ typedef struct {
     int64_t max_survivors;          /* largest per-query survivor count                  */
     int32_t retries;                /* overflow re-scans                                 */
     int32_t kernel_launches;        /* librabitq kernels launched by this call           */
-    int32_t scan_path_used;         /* 1 popc, 2 imma                                    */
+    int32_t scan_path_used;         /* 1 popc, 2 imma (CUDA-core survivor test), 3 imma with
+                                       the folded tensor-core survivor test             */
     int32_t batches;                /* internal query batches                            */
     int64_t reranked;               /* candidates whose exact distance was taken (rerank 1) */
     float dense_ms;                 /* the dense nearest-list re-rank block (tgemm_dist1), which runs on
@@ -195,6 +196,9 @@ typedef struct {
                                                  prefix sample of every probed list (the d > 128
                                                  seeding, also used when list sizes are skewed)
                                                  instead of the nearest lists; implies NO_FOLD   */
+#define RABITQ_VARIANT_PROBE_TIGHT 64u       /* nlist >= 8192: the filtered probe GEMM's sampled
+                                                 threshold at its minimum, so most rows take the
+                                                 full-row fallback (exercises that path)         */
 #define RABITQ_VARIANT_NO_FOLD 32u           /* d <= 128, tensor-core scan: survivor test on the
                                                  CUDA cores (scan_small_kernel) instead of the
                                                  tensor-core folded test (scan_fold_kernel, which

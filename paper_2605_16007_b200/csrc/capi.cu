@@ -472,7 +472,7 @@ static void search_local(const rabitq_index* idx, const float* Q, int64_t nq, in
         pf->max_survivors = stats.max_survivors;
         pf->retries = stats.retries;
         pf->kernel_launches = stats.launches;
-        pf->scan_path_used = stats.used_imma ? 2 : 1;
+        pf->scan_path_used = stats.used_imma == 2 ? 3 : stats.used_imma ? 2 : 1;
         pf->batches = stats.batches;
         pf->reranked = stats.reranked;
         pf->dense_ms = stats.dense_ms;

@@ -237,7 +237,7 @@ struct StageTimer {
     }
 };
 void rotate_probe(const rabitq_index* idx, const float* Q, int64_t nq, int nprobe, uint32_t variant, float* Qr,
-                  int32_t* probes, cudaStream_t st, int& L, StageTimer* tm);
+                  int32_t* probes, cudaStream_t st, int& L, StageTimer* tm, bool latency = false);
 void search_batch(const rabitq_index* idx, const float* Q, int64_t nq, int k, int nprobe, int M,
                   const SearchCfg& cfg, int64_t qid_base, int64_t* ids, float* dists, const DebugOut& dbg,
                   cudaStream_t st, SearchStats* stats);
