@@ -196,9 +196,6 @@ typedef struct {
                                                  prefix sample of every probed list (the d > 128
                                                  seeding, also used when list sizes are skewed)
                                                  instead of the nearest lists; implies NO_FOLD   */
-#define RABITQ_VARIANT_PROBE_TIGHT 64u       /* nlist >= 8192: the filtered probe GEMM's sampled
-                                                 threshold at its minimum, so most rows take the
-                                                 full-row fallback (exercises that path)         */
 #define RABITQ_VARIANT_NO_FOLD 32u           /* d <= 128, tensor-core scan: survivor test on the
                                                  CUDA cores (scan_small_kernel) instead of the
                                                  tensor-core folded test (scan_fold_kernel, which

@@ -322,7 +322,7 @@ __global__ __launch_bounds__(kNT, 1) void tgemm_kernel(const __grid_constant__ C
             tc::mbar_wait(&normf_bar[b], ub & 1);
             float an = 0.0f;
             if constexpr (kEpi == TG_EPI_DIST) an = __fadd_rn(anorm[(b * 2) * kBM + r], anorm[(b * 2 + 1) * kBM + r]);
-            if constexpr (kEpi != TG_EPI_DIST && kEpi != TG_EPI_ARGMIN && kEpi != TG_EPI_FILTER) {
+            if constexpr (kEpi != TG_EPI_DIST && kEpi != TG_EPI_ARGMIN) {
                 // row-major C: 32 x 32 blocks transposed through shared memory so
                 // that each store instruction writes 32 consecutive columns of a row
                 float* stg = stage + (warp - kEpiWarp0) * kStg;
@@ -346,33 +346,6 @@ __global__ __launch_bounds__(kNT, 1) void tgemm_kernel(const __grid_constant__ C
                         }
                     }
                     __syncwarp();
-                }
-                tc::fence_before_sync();
-                __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&acce_bar[b]);
-                continue;
-            }
-            if constexpr (kEpi == TG_EPI_FILTER) {
-                // probe candidates: the PROBE epilogue's distance (same rounding), appended
-                // where its orderable key is <= the row's threshold (about 3 nprobe per row)
-                const uint32_t to = rok ? __ldg(p.thr + ti.a0 + r) : 0u;
-                for (int c0 = 0; c0 < ti.n; c0 += 16) {
-                    uint32_t acc[16];
-                    tc::tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * kBN + c0), acc);
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const int col = c0 + i;
-                        if (col < ti.n) {
-                            const float d = __fmaf_rn(-2.0f, __uint_as_float(acc[i]), __ldg(p.b_norm + ti.b0 + col));
-                            const uint32_t ko = f2o(d);
-                            if (rok && ko <= to) {
-                                const int pos = atomicAdd(p.ccnt + ti.a0 + r, 1);
-                                if (pos < p.ccap)
-                                    p.cand[(ti.a0 + r) * (int64_t)p.ccap + pos] =
-                                        ((unsigned long long)ko << 32) | (unsigned long long)(ti.b0 + col);
-                            }
-                        }
-                    }
                 }
                 tc::fence_before_sync();
                 __syncwarp();
@@ -627,10 +600,6 @@ void tgemm(const TgParams& p, int epi, cudaStream_t st) {
     } else if (epi == TG_EPI_PROBE) {
         if (tma) RQ_TG(TG_EPI_PROBE, true);
         else RQ_TG(TG_EPI_PROBE, false);
-    } else if (epi == TG_EPI_FILTER) {
-        RQ_REQUIRE(p.tiles == nullptr && p.thr && p.cand && p.ccnt, RABITQ_ERR_INTERNAL, "tgemm filter: plain mode");
-        if (tma) RQ_TG(TG_EPI_FILTER, true);
-        else RQ_TG(TG_EPI_FILTER, false);
     } else if (epi == TG_EPI_ARGMIN) {
         RQ_REQUIRE(p.tiles == nullptr && p.amin != nullptr, RABITQ_ERR_INTERNAL, "tgemm argmin: plain mode");
         if (tma) RQ_TG(TG_EPI_ARGMIN, true);

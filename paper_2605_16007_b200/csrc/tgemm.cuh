@@ -5,7 +5,7 @@
 
 namespace rabitq {
 
-enum { TG_EPI_STORE = 0, TG_EPI_PROBE = 1, TG_EPI_DIST = 2, TG_EPI_ARGMIN = 3, TG_EPI_FILTER = 4 };
+enum { TG_EPI_STORE = 0, TG_EPI_PROBE = 1, TG_EPI_DIST = 2, TG_EPI_ARGMIN = 3 };
 
 // one output tile of a batched product: A rows [a0, a0 + m), B rows [b0, b0 + n)
 // (through a_idx / b_idx when given), output at C + c0 with leading dimension ldc
@@ -29,18 +29,12 @@ struct TgParams {
     int64_t ldc;             // plain mode
     const float* b_norm;     // PROBE / ARGMIN: ||c||^2 per B row; DIST: ||q||^2 per (gathered) B row id
     unsigned long long* amin;  // ARGMIN: [M] running min of (orderable(||c||^2 - 2 a.c) << 32 | B row), plain mode
-    const uint32_t* thr;       // FILTER: [M] orderable threshold per A row (plain mode)
-    unsigned long long* cand;  // FILTER: [M][ccap] (orderable(d) << 32 | B row) of every d with key <= thr
-    int* ccnt;                 // FILTER: [M] candidates appended (may exceed ccap: overflow)
-    int ccap;
 };
 
 // STORE: C = A B^T (row-major tile); PROBE: C = b_norm[col] - 2 A B^T;
 // DIST: C[col * ldc + row] = max(0, ||a_row||^2 + b_norm[b id] - 2 a.b) (column-major tile);
 // ARGMIN: amin[row] = min(amin[row], key(b_norm[col] - 2 a.b, col)) over the tile's columns
 // (k-means / list assignment: nearest centroid, ties -> lowest id; no distance matrix written)
-// FILTER: the PROBE distance d = b_norm[col] - 2 a.b of every column with f2o(d) <= thr[row] is
-// appended to cand[row] (no distance matrix written)
 void tgemm(const TgParams& p, int epi, cudaStream_t st);
 // dense re-rank block, 1xTF32 fed by TMA (plain A / B rows, p.tiles):
 // C[c0 + col ldc + row] = a_norm[a row]^2 + b_norm[b row] - 2 a.b, |error| <= 2^-8 (a_norm^2 + b_norm)
