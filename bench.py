@@ -424,6 +424,7 @@ def run_ours(args):
 
     # ---- recall@k vs exact on a query sample (torch brute force, outside the timed region) ----
     rec = None
+    gt = None
     if world == 1 and args.recall:
         nsub = min(100 if s.N <= 10_000_000 else 20, s.nq)
         step = max(1, (1 << 28) // (s.D * 4 * 8))  # rows per chunk (~1 GiB of fp32 temporaries)
@@ -479,7 +480,7 @@ def run_ours(args):
         **({"overlapped": overlapped} if overlapped else {}),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(s, idx, X, Q, args)
+        line["cpu_baseline"] = cpu_baseline(s, idx, X, Q, args, gt=gt, got=ids)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if comm is not None:
@@ -496,7 +497,7 @@ def _cores():
         return os.cpu_count() or 1
 
 
-def cpu_baseline(s, idx, X, Q, args, budget_s=20.0):
+def cpu_baseline(s, idx, X, Q, args, budget_s=20.0, gt=None, got=None):
     """The oracle as it stands, on this box's host cores, on a bounded query
     sample (about `budget_s` seconds of CPU work) over a sub-index of the lists
     those queries probe (oracle/subindex.py: the oracle's arithmetic unchanged,
@@ -513,20 +514,40 @@ def cpu_baseline(s, idx, X, Q, args, budget_s=20.0):
     Qh = Q[:nmax].cpu().numpy()
     pr = probes.cpu().numpy()
 
-    def timed(n):
+    last = {}
+
+    def timed(n, threads=cores):
         sub = SubIndex(ex, pr[:n].ravel(), lambda g: X[torch.from_numpy(g).to(X.device)].cpu().numpy())
         t0 = time.perf_counter()
-        sub.search(orc, Qh[:n], s.k, s.nprobe, s.M, s.build_seed, num_threads=cores)
+        last["ids"] = sub.search(orc, Qh[:n], s.k, s.nprobe, s.M, s.build_seed, num_threads=threads)[0]
         return time.perf_counter() - t0
 
     n0 = min(nmax, max(2, cores))
     t = timed(n0)
     n = int(min(nmax, max(n0, n0 * budget_s / max(t, 1e-3))))
     t = timed(n)
-    return {"value": round(n / t, 3), "unit": "queries/s", "cores": cores, "kind": "oracle",
-            "sample": f"first {n} of {s.nq} CFG{s.cfg} queries, full oracle path (fp64 rotate/probe, pinned fp32 "
-                      f"quantizer, plain-loop ip, fp64 estimator, full sort, fp64 re-rank) over a sub-index of their "
-                      f"probed lists, OpenMP {cores} threads, {t:.1f} s"}
+    out = {"value": round(n / t, 3), "unit": "queries/s", "cores": cores, "kind": "oracle",
+           "sample": f"first {n} of {s.nq} CFG{s.cfg} queries, full oracle path (fp64 rotate/probe, pinned fp32 "
+                     f"quantizer, plain-loop ip, fp64 estimator, full sort, fp64 re-rank) over a sub-index of their "
+                     f"probed lists, OpenMP {cores} threads, {t:.1f} s"}
+    # the oracle's recall on the bench's own recall subset (same exact kNN ground
+    # truth as recall_at_k) next to the GPU's, and the oracle at 1 thread (about budget_s / 4 s)
+    if gt is not None:
+        m = min(len(gt), n)
+        oids = np.asarray(last["ids"])[:m]
+        gids = got[:m].cpu().numpy()
+
+        def rcl(a):
+            return float(np.mean([len(set(x.tolist()) & set(y.tolist())) / s.k for x, y in zip(a, gt[:m])]))
+
+        out["recall_subset"] = {"queries": m, "oracle": round(rcl(oids), 4), "gpu": round(rcl(gids), 4),
+                                "identical_queries": round(float(np.mean([np.array_equal(np.sort(x), np.sort(y))
+                                                                          for x, y in zip(oids, gids)])), 4)}
+    n1 = int(max(1, min(n, n * (budget_s / 4) / max(t, 1e-3) / max(1, cores))))
+    t1 = timed(n1, threads=1)
+    out["value_1thread"] = round(n1 / t1, 3)
+    out["sample_1thread"] = f"first {n1} queries, 1 thread, {t1:.1f} s"
+    return out
 
 
 def reference_index(s, X, seed):
@@ -695,6 +716,8 @@ def main():
                     help="BASELINE.json configs[C-1]; default 4 = the largest single-GPU config (N = 1e8)")
     ap.add_argument("--nq", type=int, default=0, help="override the query count (quick runs)")
     ap.add_argument("--nprobe", type=int, default=0, help="override nprobe (CFG3's sweep: 16/32/64/128)")
+    ap.add_argument("--nprobe-sweep", default="", dest="nprobe_sweep",
+                    help="comma list, e.g. 16,32,64,128 (CFG3): one JSON line per nprobe from one call, same code")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--scan-path", type=int, default=0, dest="scan_path")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -724,6 +747,11 @@ def main():
         run_build(args)
     elif args.impl == "reference":
         run_reference(args)
+    elif args.nprobe_sweep:
+        for npb in [int(x) for x in args.nprobe_sweep.split(",") if x]:
+            args.nprobe = npb
+            run_ours(args)
+            torch.cuda.empty_cache()
     else:
         run_ours(args)
 
