@@ -421,6 +421,14 @@ def run_ours(args):
                  "pairs": pairs,
                  "hbm_equiv_gbs": round(scan_bytes / (stage_ms["scan"] * 1e-3) / 1e9, 1),
                  "bytes_per_pair": 4 * W + 8, "ms": round(stage_ms["scan"], 4)}
+    if fold:
+        # the folded scan reads one f32 accumulator per pair from TMEM: against the read rate
+        # tools/ubench/tmem_ld.cu measures (375 B per clock and SM with >= 12 reading warps,
+        # profiles/r2c/tmem_ld.txt) -- not the bound, stated so that the bound is named by measurement
+        tm_peak = 375.0 * 148 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e9
+        scan_roof["tmem_read"] = {"achieved_gbs": round(pairs * 4 / (stage_ms["scan"] * 1e-3) / 1e9, 1),
+                                  "peak_gbs": round(tm_peak, 1),
+                                  "frac": round(pairs * 4 / (stage_ms["scan"] * 1e-3) / 1e9 / tm_peak, 4)}
 
     # ---- recall@k vs exact on a query sample (torch brute force, outside the timed region) ----
     rec = None

@@ -1285,13 +1285,28 @@ __global__ __launch_bounds__(kSkNT, 1) void scan_small_kernel(const __grid_const
 // scan's exact key.  A stages carry the tile's codes (TMA) and its X rows (16
 // tf32 per vector, written by 4 producer warps from the tile's row
 // constants); the row constants live in a per-tile ring.
-constexpr int kFxTS = 4;                    // TMEM slots (units in flight), 128 columns each
-constexpr int kFxUW = 128;                  // unit width: a tile's group is split into <= 2 column halves
+#ifndef FX_UW
+#define FX_UW 128
+#endif
+#ifndef FX_EPIW
+#define FX_EPIW 12
+#endif
+#ifndef FX_GATE
+#define FX_GATE 0
+#endif
+#ifndef FX_NS0
+#define FX_NS0 32
+#endif
+#ifndef FX_NSMAX
+#define FX_NSMAX 256
+#endif
+constexpr int kFxUW = FX_UW;                // unit width: a tile's group is split into <= 256 / kFxUW column parts
+constexpr int kFxTS = kTmemCols / kFxUW;    // TMEM slots (units in flight), kFxUW columns each
 #ifndef FX_SA
 #define FX_SA 4
 #endif
 #ifndef FX_RT
-#define FX_RT 8
+#define FX_RT (FX_SA + 512 / FX_UW)
 #endif
 #ifndef FX_RI
 #define FX_RI 6
@@ -1299,7 +1314,7 @@ constexpr int kFxUW = 128;                  // unit width: a tile's group is spl
 constexpr int kFxSA = FX_SA;                // A stages (codes 16 KB + X 8 KB)
 constexpr int kFxRT = FX_RT;                // row-constant ring (tiles)
 constexpr int kFxRI = FX_RI;                // item records
-constexpr int kFxEpiW = 12;                 // epilogue warps (3 per TMEM lane quarter)
+constexpr int kFxEpiW = FX_EPIW;            // epilogue warps (kFxEpiW / 4 per TMEM lane quarter)
 constexpr int kFxXW = 4;                    // X producer warps (one vector row per lane)
 constexpr int kFxMmaW = 2 + kFxXW;          // warps 0 sched + B, 1 A loader, 2..5 X producers, 6 MMA
 constexpr int kFxEpi0 = kFxMmaW + 1;
@@ -1315,7 +1330,14 @@ constexpr uint32_t kFxOffR = kFxOffA + kFxSA * kFxAStage;
 constexpr uint32_t kFxSmem = kFxOffR + kFxRT * sizeof(SkRows) + 1024;
 static_assert(kFxSmem <= 227 * 1024, "fold scan shared memory");
 static_assert(kFxOffA % 1024 == 0 && kFxAStage % 1024 == 0, "A stages 1024-aligned (128-byte swizzle)");
-static_assert(kFxTS * kFxUW <= kTmemCols, "fold scan TMEM");
+static_assert(kFxTS * kFxUW <= kTmemCols && kFxUW <= 8 * kEC, "fold scan TMEM (<= 8 chunks per unit: rb0 / rb1)");
+static_assert(kFxEpiW % 4 == 0 && kFxEpiW / 4 <= kFxTS + 1, "fold scan: accf parity argument (epilogue warps per quarter)");
+
+// units of a group of nc columns: nu parts of wu (multiple of 16, <= kFxUW) columns
+__device__ __forceinline__ void fx_units(int nc, int& nu, int& wu) {
+    nu = (nc + kFxUW - 1) / kFxUW;
+    wu = nu == 1 ? ((nc + 15) & ~15) : (((nc + nu - 1) / nu + 15) & ~15);
+}
 
 // exact ip of code row x query row (both e4m3 bytes in the grouped scan's K
 // order, codes 0xB8 = -1 / 0, queries 0..15): the flagged pairs' key input
@@ -1357,7 +1379,7 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
     __shared__ uint32_t next_chunk[4];
     __shared__ uint32_t mma_issued;  // tiles whose MMAs the MMA warp has issued (epilogue wait gate)
     __shared__ __align__(8) uint64_t ifull[kFxRI], iempty[kFxRI], bfull[2], bfree[2], afull[kFxSA], xfull[kFxSA],
-        aempty[kFxSA], accf[kFxTS], acce[kFxTS], rowf[kFxRT];
+        aempty[kFxSA], accf[2 * kFxTS], acce[kFxTS], rowf[kFxRT];
     __shared__ uint32_t tmem_base_s;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (warp == kFxMmaW) tc::tmem_alloc(&tmem_base_s, kTmemCols);
@@ -1377,6 +1399,7 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
         }
         for (int k = 0; k < kFxTS; ++k) {
             tc::mbar_init(&accf[k], 1);
+            tc::mbar_init(&accf[kFxTS + k], 1);
             tc::mbar_init(&acce[k], 4);  // one warp per TMEM lane quarter
         }
         for (int t = 0; t < kFxRT; ++t) tc::mbar_init(&rowf[t], 1);
@@ -1511,8 +1534,8 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
             if (r.w == 0) break;
             const int nc = r.w & 511, nt = (r.w >> 9) & 15;
             // units: the group's columns in nu <= 2 halves of wu (multiple of 16) columns
-            const int nu = nc > kFxUW ? 2 : 1;
-            const int wu = nu == 1 ? ((nc + 15) & ~15) : ((((nc + 1) >> 1) + 15) & ~15);
+            int nu, wu;
+            fx_units(nc, nu, wu);
             const int wl = ((nc - (nu - 1) * wu) + 15) & ~15;  // last unit's MMA width
             const uint32_t id8 = tc::idesc_f8(kTM, wu), id32 = tc::idesc_tf32_f32(kTM, wu);
             const uint32_t id8l = tc::idesc_f8(kTM, wl), id32l = tc::idesc_tf32_f32(kTM, wl);
@@ -1539,8 +1562,15 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
                     const bool last = u == nu - 1;
                     // B rows [u wu, +wu): wu x 128 B (SW128: 16-byte descriptor units); BX: wu / 8 x 512 B
                     tc::mma_fold_acc_w<NK>(dt, adesc, bdesc + (uint64_t)(u * wu * 8), last ? id8l : id8, xdesc,
-                                           bxdesc + (uint64_t)(u * wu * 4), last ? id32l : id32, accf_s + 8u * k);
+                                           bxdesc + (uint64_t)(u * wu * 4), last ? id32l : id32,
+#if FX_GATE
+                                           accf_s + 8u * k);
+#else
+                                           accf_s + 8u * (ucnt % (2u * kFxTS)));
+#endif
+#if FX_GATE
                     if (lane == 0) atomicExch(&mma_issued, ucnt + 1u);
+#endif
                 }
                 tc::commit_warp(&aempty[as]);                // the tile's codes and X rows are free
                 if (t == nt - 1) tc::commit_warp(&bfree[b]);  // the item's B and BX are free
@@ -1570,8 +1600,7 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
                         break;
                     }
                     const int nc_ = R.w & 511;
-                    nu = nc_ > kFxUW ? 2 : 1;
-                    wu = nu == 1 ? ((nc_ + 15) & ~15) : ((((nc_ + 1) >> 1) + 15) & ~15);
+                    fx_units(nc_, nu, wu);
                     nut = ((R.w >> 9) & 15) * nu;
                 }
                 if (uc < u0 + (uint32_t)nut) break;
@@ -1585,115 +1614,147 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
             if (done) break;
             const int nc = R.w & 511, t0 = (int)((uint32_t)R.w >> 13);
             const int x = (int)(uc - u0);
-            const int t = nu == 1 ? x : x >> 1, u = x - t * nu;
+            // x / nu for nu in 1..4 without an integer division (x < 8 * 4)
+            const int t = nu == 1 ? x : nu == 2 ? x >> 1 : nu == 4 ? x >> 2 : (x * 43) >> 7, u = x - t * nu;
             const int64_t v = (int64_t)(t0 + t) * kTM + r;
             const bool vok = v < R.y;
             const uint32_t tcnt = tc0 + (uint32_t)t;
             const uint32_t k = uc % kFxTS;
             const int cend = min(nc, (u + 1) * wu) - u * wu;  // valid columns of the unit
             if (lane == 0) FX_CRUMB(10 + (warp - kFxEpi0), ((long long)uc << 32) | (uint32_t)cend);
+#if FX_GATE
             // Once the MMA warp has issued unit uc, the slot's previous fill has completed
             // (issue waited for its release), so the accf parity wait is unambiguous however
             // far ahead of the MMA this warp took its unit; the tile's rowf phase is complete
             // by then as well (its X rows were consumed).
             if (*(volatile uint32_t*)&mma_issued <= uc) {
-                uint32_t ns = 32;
+                uint32_t ns = FX_NS0;
                 while (*(volatile uint32_t*)&mma_issued <= uc) {
                     __nanosleep(ns);
-                    if (ns < 256) ns <<= 1;
+                    if (ns < FX_NSMAX) ns <<= 1;
                 }
             }
             tc::mbar_wait_s(accf_s + 8u * k, (uc / kFxTS) & 1);
+#else
+            // No gate, no polling: unit uc's commit arrives on accf[uc % (2 TS)], two barriers per
+            // TMEM slot used alternately, so the parity wait can only confuse "uc complete" with
+            // "uc - 2 TS still in flight" -- and unit uc - 2 TS is finished when a warp takes uc:
+            // the quarter's warps take units in order and hold one each; were uc - 2 TS unfinished,
+            // its slot would not have been released, the MMA warp would be blocked before unit
+            // uc - TS, and units uc - 2 TS and uc - TS .. uc - 1 (TS + 1 of them) would all be held
+            // by the quarter's other kFxEpiW / 4 - 1 < TS + 1 warps.
+            tc::mbar_wait_s(accf_s + 8u * (uc % (2u * kFxTS)), (uc / (2u * kFxTS)) & 1);
+#endif
             __syncwarp();  // reconverge before tcgen05.ld.sync.aligned
             tc::fence_after_sync();
             const uint32_t tb = lane_base + k * (uint32_t)kFxUW;
-            bool rows_ready = false;
+            // Fast pass: the sign bits of the unit's accumulators.  Flagged chunks leave their
+            // per-row bits (16 per chunk) in rb0 / rb1; the slot is released before the slow
+            // path runs, which needs only those bits and the row's constants (ncu: with the slow
+            // path inside, a flagged chunk -- about one quarter-unit in ten at CFG4 -- held its
+            // accumulator slot for the latency of its global loads and atomics, and the MMA
+            // warp, 4 slots ahead at most, waited on it)
+            uint64_t rb0 = 0ull, rb1 = 0ull;  // chunks 0-3 and 4-7 of the unit
+            uint32_t flagged = 0u;            // warp-uniform: chunk j has a flagged pair
             for (int c2 = 0; c2 < cend; c2 += 4 * kEC) {
                 // 64 columns per wait (4 loads in flight); columns past the unit's width
                 // read the slot's unused columns and are masked below
+                uint32_t d2[4][kEC];
+                tc::tmem_ld16_nw(tb + (uint32_t)c2, d2[0]);
+                tc::tmem_ld16_nw(tb + (uint32_t)(c2 + kEC), d2[1]);
+                tc::tmem_ld16_nw(tb + (uint32_t)(c2 + 2 * kEC), d2[2]);
+                tc::tmem_ld16_nw(tb + (uint32_t)(c2 + 3 * kEC), d2[3]);
+                tc::tmem_ld_wait();
                 uint32_t flag4 = 0u;
-                {
-                    uint32_t d2[4][kEC];
-                    tc::tmem_ld16_nw(tb + (uint32_t)c2, d2[0]);
-                    tc::tmem_ld16_nw(tb + (uint32_t)(c2 + kEC), d2[1]);
-                    tc::tmem_ld16_nw(tb + (uint32_t)(c2 + 2 * kEC), d2[2]);
-                    tc::tmem_ld16_nw(tb + (uint32_t)(c2 + 3 * kEC), d2[3]);
-                    tc::tmem_ld_wait();
 #pragma unroll
-                    for (int hh = 0; hh < 4; ++hh) {
-                        uint32_t any = d2[hh][0];
+                for (int hh = 0; hh < 4; ++hh) {
+                    uint32_t any = d2[hh][0];
 #pragma unroll
-                        for (int c = 1; c < kEC; ++c) any |= d2[hh][c];
-                        flag4 |= (vok && (any >> 31) && c2 + hh * kEC < cend) ? (1u << hh) : 0u;
-                    }
+                    for (int c = 1; c < kEC; ++c) any |= d2[hh][c];
+                    flag4 |= (vok && (any >> 31) && c2 + hh * kEC < cend) ? (1u << hh) : 0u;
                 }
                 flag4 = __reduce_or_sync(0xFFFFFFFFu, flag4);
-#ifdef RABITQ_DIAG
-                if (a.fold_diag >= 8) {  // pure delay instead of the slow path (race hunting)
-                    if (flag4) __nanosleep(a.fold_diag == 9 ? 20000 : 2000);
-                    continue;
-                }
-                if (a.fold_diag == 1) continue;
-#endif
-                for (uint32_t f4 = flag4; f4; f4 &= f4 - 1) {
-                    const int hh = __ffs(f4) - 1;
-                    const int cl0 = c2 + hh * kEC;  // unit column of the chunk
-                    uint32_t d[kEC];
-                    tc::tmem_ld16(tb + (uint32_t)cl0, d);  // re-read the flagged chunk (rare)
-                    // ---- slow path: exact keys of the flagged pairs of this chunk ----
-                    const int rt = (int)(tcnt % kFxRT);
-                    if (!rows_ready) {
-                        tc::mbar_wait_s(rowf_s + 8u * rt, (tcnt / kFxRT) & 1);
-                        rows_ready = true;
-                    }
-                    const SkRows& RS = urows[rt];
-                    const float2 fac = vok ? RS.fac[r] : make_float2(0.f, 0.f);
-                    const float pcf = vok ? (float)RS.pcnt[r] : 0.f;
-                    const uint32_t row = vok ? RS.rows[r] : 0u;
-                    uint32_t rowbits = 0u;
+                if (flag4) {  // rare
+                    uint64_t rb = 0ull;
 #pragma unroll
-                    for (int c = kEC - 1; c >= 0; --c) rowbits = (rowbits << 1) | (d[c] >> 31);
-                    const int rem = cend - cl0;
-                    if (rem < kEC) rowbits &= (1u << rem) - 1u;
-                    if (!vok) rowbits = 0u;
-                    const uint32_t cols = __reduce_or_sync(0xFFFFFFFFu, rowbits);
-                    // lane c < 16 owns column c: its row ballot, constants and counter atomic
-                    uint32_t mybal = 0u;
-                    for (uint32_t m = cols; m; m &= m - 1) {
-                        const int i2 = __ffs(m) - 1;
-                        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, (rowbits >> i2) & 1u);
-                        if (lane == i2) mybal = bal;
-                    }
-                    const int64_t gcol0 = (int64_t)R.z + u * wu + cl0;  // grouped row of the chunk's column 0
-                    ColC mc{};
-                    int mybase = 0;
-                    if (mybal) {
-                        mc = colp_get(a.gcolp, (int)(gcol0 + lane));
-                        mybase = atomicAdd(&a.cnt[mc.q], __popc(mybal));
-                    }
-                    const uint8_t* crow = a.codes8 + (size_t)(R.x + v) * a.Dp;
-                    for (uint32_t m = cols; m; m &= m - 1) {
-                        const int i2 = __ffs(m) - 1;
-                        const uint32_t bal = __shfl_sync(0xFFFFFFFFu, mybal, i2);
-                        const int base = __shfl_sync(0xFFFFFFFFu, mybase, i2);
-                        ColC cq;
-                        cq.a = __shfl_sync(0xFFFFFFFFu, mc.a, i2);
-                        cq.b = __shfl_sync(0xFFFFFFFFu, mc.b, i2);
-                        cq.K = __shfl_sync(0xFFFFFFFFu, mc.K, i2);
-                        cq.nq2 = __shfl_sync(0xFFFFFFFFu, mc.nq2, i2);
-                        cq.q = __shfl_sync(0xFFFFFFFFu, mc.q, i2);
-                        if ((bal >> lane) & 1u) {
-                            const float ipn = ipn_rows(crow, a.qbar8 + (size_t)(gcol0 + i2) * a.Dp, a.Dp);
-                            const float key = est_of<true>(__float_as_uint(ipn), cq, fac, pcf);
-                            const int pos = base + __popc(bal & ((1u << lane) - 1u));
-                            if (pos < a.cap) a.buf[(size_t)cq.q * a.cap + pos] = make_key(key, row);
+                    for (int hh = 0; hh < 4; ++hh) {
+                        if ((flag4 >> hh) & 1u) {
+                            uint32_t rowbits = 0u;
+#pragma unroll
+                            for (int c = kEC - 1; c >= 0; --c) rowbits = (rowbits << 1) | (d2[hh][c] >> 31);
+                            const int rem = cend - (c2 + hh * kEC);
+                            if (rem < kEC) rowbits &= (1u << rem) - 1u;
+                            if (!vok) rowbits = 0u;
+                            rb |= (uint64_t)rowbits << (16 * hh);
                         }
                     }
+                    if (c2 == 0) rb0 = rb;
+                    else rb1 = rb;
+                    flagged |= flag4 << (c2 >> 4);
+                }
+            }
+#ifdef RABITQ_DIAG
+            if (a.fold_diag >= 8) {  // pure delay instead of the slow path (race hunting)
+                if (flagged) __nanosleep(a.fold_diag == 9 ? 20000 : 2000);
+                flagged = 0u;
+            }
+            if (a.fold_diag == 1) flagged = 0u;
+#endif
+            float2 fac = make_float2(0.f, 0.f);
+            float pcf = 0.f;
+            uint32_t row = 0u;
+            if (flagged) {
+                const int rt = (int)(tcnt % kFxRT);
+                tc::mbar_wait_s(rowf_s + 8u * rt, (tcnt / kFxRT) & 1);
+                const SkRows& RS = urows[rt];
+                if (vok) {
+                    fac = RS.fac[r];
+                    pcf = (float)RS.pcnt[r];
+                    row = RS.rows[r];
                 }
             }
             tc::fence_before_sync();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive_s(acce_s + 8u * k);  // the slot may be refilled
+            if (lane == 0) tc::mbar_arrive_s(acce_s + 8u * k);  // the slot (and its row constants) may be refilled
+            // ---- slow path: exact keys of the flagged pairs, chunk by chunk ----
+            for (uint32_t f = flagged; f; f &= f - 1) {
+                const int j = __ffs(f) - 1;
+                const int cl0 = j * kEC;  // unit column of the chunk
+                const uint32_t rowbits = (uint32_t)((j < 4 ? rb0 : rb1) >> (16 * (j & 3))) & 0xFFFFu;
+                const uint32_t cols = __reduce_or_sync(0xFFFFFFFFu, rowbits);
+                // lane c < 16 owns column c: its row ballot, constants and counter atomic
+                uint32_t mybal = 0u;
+                for (uint32_t m = cols; m; m &= m - 1) {
+                    const int i2 = __ffs(m) - 1;
+                    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, (rowbits >> i2) & 1u);
+                    if (lane == i2) mybal = bal;
+                }
+                const int64_t gcol0 = (int64_t)R.z + u * wu + cl0;  // grouped row of the chunk's column 0
+                ColC mc{};
+                int mybase = 0;
+                if (mybal) {
+                    mc = colp_get(a.gcolp, (int)(gcol0 + lane));
+                    mybase = atomicAdd(&a.cnt[mc.q], __popc(mybal));
+                }
+                const uint8_t* crow = a.codes8 + (size_t)(R.x + v) * a.Dp;
+                for (uint32_t m = cols; m; m &= m - 1) {
+                    const int i2 = __ffs(m) - 1;
+                    const uint32_t bal = __shfl_sync(0xFFFFFFFFu, mybal, i2);
+                    const int base = __shfl_sync(0xFFFFFFFFu, mybase, i2);
+                    ColC cq;
+                    cq.a = __shfl_sync(0xFFFFFFFFu, mc.a, i2);
+                    cq.b = __shfl_sync(0xFFFFFFFFu, mc.b, i2);
+                    cq.K = __shfl_sync(0xFFFFFFFFu, mc.K, i2);
+                    cq.nq2 = __shfl_sync(0xFFFFFFFFu, mc.nq2, i2);
+                    cq.q = __shfl_sync(0xFFFFFFFFu, mc.q, i2);
+                    if ((bal >> lane) & 1u) {
+                        const float ipn = ipn_rows(crow, a.qbar8 + (size_t)(gcol0 + i2) * a.Dp, a.Dp);
+                        const float key = est_of<true>(__float_as_uint(ipn), cq, fac, pcf);
+                        const int pos = base + __popc(bal & ((1u << lane) - 1u));
+                        if (pos < a.cap) a.buf[(size_t)cq.q * a.cap + pos] = make_key(key, row);
+                    }
+                }
+            }
         }
     }
     if (lane == 0) FX_CRUMB(24, warp);
