@@ -1360,6 +1360,43 @@ __device__ __forceinline__ float ipn_rows(const uint8_t* __restrict__ crow, cons
     return -((a.x + a.y) + (b.x + b.y));  // -ip (the f8 accumulator's value), exact
 }
 
+// Fast pass over N 16-column chunks of a unit (one TMEM wait): the sign bits of the accumulators.
+// Returns the warp-uniform mask of chunks holding a flagged pair; their per-row bits (16 per
+// chunk, columns >= ncols and invalid rows cleared) are OR-ed into rb.  N is a template parameter
+// so that the registers of the read are a static array (predicated loads into one 4-chunk array
+// spilled 176 bytes and doubled the scan time).
+template <int N>
+__device__ __forceinline__ uint32_t fx_pass(uint32_t taddr, bool vok, int ncols, uint64_t& rb) {
+    uint32_t d2[N][kEC];
+#pragma unroll
+    for (int hh = 0; hh < N; ++hh) tc::tmem_ld16_nw(taddr + (uint32_t)(hh * kEC), d2[hh]);
+    tc::tmem_ld_wait();
+    uint32_t flag4 = 0u;
+#pragma unroll
+    for (int hh = 0; hh < N; ++hh) {
+        uint32_t any = d2[hh][0];
+#pragma unroll
+        for (int c = 1; c < kEC; ++c) any |= d2[hh][c];
+        flag4 |= (vok && (any >> 31)) ? (1u << hh) : 0u;
+    }
+    flag4 = __reduce_or_sync(0xFFFFFFFFu, flag4);
+    if (flag4) {  // rare
+#pragma unroll
+        for (int hh = 0; hh < N; ++hh) {
+            if ((flag4 >> hh) & 1u) {
+                uint32_t rowbits = 0u;
+#pragma unroll
+                for (int c = kEC - 1; c >= 0; --c) rowbits = (rowbits << 1) | (d2[hh][c] >> 31);
+                const int rem = ncols - hh * kEC;
+                if (rem < kEC) rowbits &= (1u << rem) - 1u;
+                if (!vok) rowbits = 0u;
+                rb |= (uint64_t)rowbits << (16 * hh);
+            }
+        }
+    }
+    return flag4;
+}
+
 template <int NK>
 __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_constant__ CUtensorMap tmapB,
                                                              const __grid_constant__ CUtensorMap tmapA, ScanArgs a,
@@ -1369,8 +1406,15 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
 #ifdef RABITQ_DIAG
     volatile long long* crumb = a.trace ? (volatile long long*)a.trace + (size_t)blockIdx.x * 32 : nullptr;
 #define FX_CRUMB(slot, val) do { if (crumb) crumb[slot] = (long long)(val); } while (0)
+    // timeline of CTA 0 (one lane per event): event ev of tile / unit idx < 1024
+#define FX_TL(ev, idx)                                                                   \
+    do {                                                                                  \
+        if (a.fold_tl && blockIdx.x == 0 && (uint32_t)(idx) < 1024u)                      \
+            a.fold_tl[(ev) * 1024 + (int)(idx)] = clock64();                              \
+    } while (0)
 #else
 #define FX_CRUMB(slot, val) do { } while (0)
+#define FX_TL(ev, idx) do { } while (0)
 #endif
     const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
     uint8_t* smem = smem_raw + pad;  // [2] B | [2] BX | [kFxSA] (codes | X) | [kFxRT] row constants
@@ -1457,6 +1501,7 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
                     const int st = (int)(tcnt % kFxSA);
                     if (tcnt >= (uint32_t)kFxSA) tc::mbar_wait(&aempty[st], ((tcnt / kFxSA) - 1) & 1);
                     FX_CRUMB(1, tcnt);
+                    FX_TL(0, tcnt);
                     tc::mbar_arrive_expect_tx(&afull[st], (uint32_t)kAStage);
                     tc::tma_load_2d(smem + kFxOffA + st * kFxAStage, &tmapA, &afull[st], 0, r.x + (t0 + t) * kTM);
                     // row constants of tile tcnt: slot tcnt % 8 was last used by tile tcnt - 8,
@@ -1493,6 +1538,7 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
                 tc::mbar_wait(&rowf[rt], (tcnt / kFxRT) & 1);
                 const SkRows& R = urows[rt];
                 if (lane == 0) FX_CRUMB(2 + (warp - 2), tcnt);
+                if (lane == 0 && warp == 2) FX_TL(1, tcnt);
                 uint8_t* xs = smem + kFxOffA + st * kFxAStage + kAStage;
                 const int nv = r.y - (t0 + t) * kTM;
                 float pc = 0.f, ah = 0.f, al = 0.f, bh = 0.f, bl = 0.f;
@@ -1519,6 +1565,7 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
                 tc::fence_proxy_async();
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&xfull[st]);
+                if (lane == 0 && warp == 2) FX_TL(2, tcnt);
             }
         }
     } else if (warp == kFxMmaW) {
@@ -1550,6 +1597,7 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
                 const int as = (int)(tcnt % kFxSA);
                 tc::mbar_wait(&afull[as], (tcnt / kFxSA) & 1);
                 tc::mbar_wait(&xfull[as], (tcnt / kFxSA) & 1);
+                if (lane == 0) FX_TL(3, tcnt);
                 const uint32_t abase = tc::smem_u32(smem + kFxOffA + as * kFxAStage);
                 const uint64_t adesc = tc::smem_desc_sw128(abase), xdesc = tc::smem_desc(abase + kAStage, 128, 512);
 #pragma unroll 1
@@ -1557,6 +1605,7 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
                     const uint32_t k = ucnt % kFxTS;
                     if (ucnt >= (uint32_t)kFxTS) tc::mbar_wait_s(acce_s + 8u * k, ((ucnt / kFxTS) - 1) & 1);
                     __syncwarp();  // the waits loop per thread: reconverge before elect.sync / tcgen05
+                    if (lane == 0) FX_TL(4, ucnt);
                     tc::fence_after_sync();
                     const uint32_t dt = tmem + k * (uint32_t)kFxUW;
                     const bool last = u == nu - 1;
@@ -1571,6 +1620,7 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
 #if FX_GATE
                     if (lane == 0) atomicExch(&mma_issued, ucnt + 1u);
 #endif
+                    if (lane == 0) FX_TL(5, ucnt);
                 }
                 tc::commit_warp(&aempty[as]);                // the tile's codes and X rows are free
                 if (t == nt - 1) tc::commit_warp(&bfree[b]);  // the item's B and BX are free
@@ -1622,6 +1672,7 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
             const uint32_t k = uc % kFxTS;
             const int cend = min(nc, (u + 1) * wu) - u * wu;  // valid columns of the unit
             if (lane == 0) FX_CRUMB(10 + (warp - kFxEpi0), ((long long)uc << 32) | (uint32_t)cend);
+            if (lane == 0 && quarter == 0) FX_TL(6, uc);
 #if FX_GATE
             // Once the MMA warp has issued unit uc, the slot's previous fill has completed
             // (issue waited for its release), so the accf parity wait is unambiguous however
@@ -1646,6 +1697,7 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
             tc::mbar_wait_s(accf_s + 8u * (uc % (2u * kFxTS)), (uc / (2u * kFxTS)) & 1);
 #endif
             __syncwarp();  // reconverge before tcgen05.ld.sync.aligned
+            if (lane == 0 && quarter == 0) FX_TL(7, uc);
             tc::fence_after_sync();
             const uint32_t tb = lane_base + k * (uint32_t)kFxUW;
             // Fast pass: the sign bits of the unit's accumulators.  Flagged chunks leave their
@@ -1657,37 +1709,16 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
             uint64_t rb0 = 0ull, rb1 = 0ull;  // chunks 0-3 and 4-7 of the unit
             uint32_t flagged = 0u;            // warp-uniform: chunk j has a flagged pair
             for (int c2 = 0; c2 < cend; c2 += 4 * kEC) {
-                // 64 columns per wait (4 loads in flight); columns past the unit's width
-                // read the slot's unused columns and are masked below
-                uint32_t d2[4][kEC];
-                tc::tmem_ld16_nw(tb + (uint32_t)c2, d2[0]);
-                tc::tmem_ld16_nw(tb + (uint32_t)(c2 + kEC), d2[1]);
-                tc::tmem_ld16_nw(tb + (uint32_t)(c2 + 2 * kEC), d2[2]);
-                tc::tmem_ld16_nw(tb + (uint32_t)(c2 + 3 * kEC), d2[3]);
-                tc::tmem_ld_wait();
-                uint32_t flag4 = 0u;
-#pragma unroll
-                for (int hh = 0; hh < 4; ++hh) {
-                    uint32_t any = d2[hh][0];
-#pragma unroll
-                    for (int c = 1; c < kEC; ++c) any |= d2[hh][c];
-                    flag4 |= (vok && (any >> 31) && c2 + hh * kEC < cend) ? (1u << hh) : 0u;
-                }
-                flag4 = __reduce_or_sync(0xFFFFFFFFu, flag4);
-                if (flag4) {  // rare
-                    uint64_t rb = 0ull;
-#pragma unroll
-                    for (int hh = 0; hh < 4; ++hh) {
-                        if ((flag4 >> hh) & 1u) {
-                            uint32_t rowbits = 0u;
-#pragma unroll
-                            for (int c = kEC - 1; c >= 0; --c) rowbits = (rowbits << 1) | (d2[hh][c] >> 31);
-                            const int rem = cend - (c2 + hh * kEC);
-                            if (rem < kEC) rowbits &= (1u << rem) - 1u;
-                            if (!vok) rowbits = 0u;
-                            rb |= (uint64_t)rowbits << (16 * hh);
-                        }
-                    }
+                // <= 64 columns per wait, only the unit's valid 16-column chunks (the epilogue
+                // warps set the kernel's pace: every instruction per unit counts)
+                const int ncols = cend - c2;
+                uint64_t rb = 0ull;
+                uint32_t flag4;
+                if (ncols > 3 * kEC) flag4 = fx_pass<4>(tb + (uint32_t)c2, vok, ncols, rb);
+                else if (ncols > 2 * kEC) flag4 = fx_pass<3>(tb + (uint32_t)c2, vok, ncols, rb);
+                else if (ncols > kEC) flag4 = fx_pass<2>(tb + (uint32_t)c2, vok, ncols, rb);
+                else flag4 = fx_pass<1>(tb + (uint32_t)c2, vok, ncols, rb);
+                if (flag4) {
                     if (c2 == 0) rb0 = rb;
                     else rb1 = rb;
                     flagged |= flag4 << (c2 >> 4);
@@ -1699,6 +1730,7 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
                 flagged = 0u;
             }
             if (a.fold_diag == 1) flagged = 0u;
+            if (lane == 0 && quarter == 0 && flagged) FX_TL(12, uc);
 #endif
             float2 fac = make_float2(0.f, 0.f);
             float pcf = 0.f;
@@ -1716,6 +1748,7 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
             tc::fence_before_sync();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive_s(acce_s + 8u * k);  // the slot (and its row constants) may be refilled
+            if (lane == 0) FX_TL(8 + quarter, uc);
             // ---- slow path: exact keys of the flagged pairs, chunk by chunk ----
             for (uint32_t f = flagged; f; f &= f - 1) {
                 const int j = __ffs(f) - 1;
@@ -1730,13 +1763,17 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
                     if (lane == i2) mybal = bal;
                 }
                 const int64_t gcol0 = (int64_t)R.z + u * wu + cl0;  // grouped row of the chunk's column 0
+                // memory-level parallelism: the column constants (owner lanes) and the code / query
+                // rows of each row's first flagged column are loaded together; the counter atomic,
+                // which needs the constants' q, is issued once they are back
                 ColC mc{};
                 int mybase = 0;
-                if (mybal) {
-                    mc = colp_get(a.gcolp, (int)(gcol0 + lane));
-                    mybase = atomicAdd(&a.cnt[mc.q], __popc(mybal));
-                }
+                if (mybal) mc = colp_get(a.gcolp, (int)(gcol0 + lane));
                 const uint8_t* crow = a.codes8 + (size_t)(R.x + v) * a.Dp;
+                const int i2f = rowbits ? __ffs(rowbits) - 1 : -1;
+                float ipn0 = 0.f;
+                if (i2f >= 0) ipn0 = ipn_rows(crow, a.qbar8 + (size_t)(gcol0 + i2f) * a.Dp, a.Dp);
+                if (mybal) mybase = atomicAdd(&a.cnt[mc.q], __popc(mybal));
                 for (uint32_t m = cols; m; m &= m - 1) {
                     const int i2 = __ffs(m) - 1;
                     const uint32_t bal = __shfl_sync(0xFFFFFFFFu, mybal, i2);
@@ -1748,7 +1785,7 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
                     cq.nq2 = __shfl_sync(0xFFFFFFFFu, mc.nq2, i2);
                     cq.q = __shfl_sync(0xFFFFFFFFu, mc.q, i2);
                     if ((bal >> lane) & 1u) {
-                        const float ipn = ipn_rows(crow, a.qbar8 + (size_t)(gcol0 + i2) * a.Dp, a.Dp);
+                        const float ipn = i2 == i2f ? ipn0 : ipn_rows(crow, a.qbar8 + (size_t)(gcol0 + i2) * a.Dp, a.Dp);
                         const float key = est_of<true>(__float_as_uint(ipn), cq, fac, pcf);
                         const int pos = base + __popc(bal & ((1u << lane) - 1u));
                         if (pos < a.cap) a.buf[(size_t)cq.q * a.cap + pos] = make_key(key, row);
@@ -1763,6 +1800,7 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
     if (tid == 0) FX_CRUMB(25, 1);
     if (warp == kFxMmaW) tc::tmem_dealloc(tmem, kTmemCols);
 #undef FX_CRUMB
+#undef FX_TL
 }
 
 }  // namespace
@@ -1950,6 +1988,15 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
                 RQ_CUDA(cudaHostGetDevicePointer(&dptr, crumbs_h, 0));
                 a.trace = dptr;
             }
+            long long* tl_h = nullptr;
+            const char* tl_path = rq_diag_env("RABITQ_FOLD_TIMELINE");
+            if (tl_path) {
+                RQ_CUDA(cudaHostAlloc(&tl_h, (size_t)16 * 1024 * sizeof(long long), cudaHostAllocMapped));
+                std::memset(tl_h, 0, (size_t)16 * 1024 * sizeof(long long));
+                long long* dptr = nullptr;
+                RQ_CUDA(cudaHostGetDevicePointer(&dptr, tl_h, 0));
+                a.fold_tl = dptr;
+            }
 #define RQ_FOLD(NK)                                                                                          \
     do {                                                                                                       \
         RQ_CUDA(cudaFuncSetAttribute(scan_fold_kernel<NK>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
@@ -1963,6 +2010,14 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
                 default: RQ_FOLD(4); break;
             }
 #undef RQ_FOLD
+            if (tl_h) {
+                const cudaError_t e = cudaStreamSynchronize(st);
+                if (FILE* f = fopen(tl_path, "wb")) {
+                    fwrite(tl_h, sizeof(long long), (size_t)16 * 1024, f);
+                    fclose(f);
+                }
+                RQ_CUDA(e);
+            }
             if (crumbs_h) {
                 const cudaError_t e = cudaStreamSynchronize(st);
                 if (FILE* f = fopen(crumbs_path, "wb")) {

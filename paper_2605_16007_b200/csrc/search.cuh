@@ -76,6 +76,7 @@ struct ScanArgs {
     int f8;                     // 1: e4m3 operands (.kind::f8f6f4): Dp <= 128, 4-bit query (codes8 / qbar8 bytes)
     int64_t items_bound;        // upper bound on the grouping's work items (small-K item table)
     int fold;                   // 1: the small-K main scan tests survivors on the tensor cores (scan_fold_kernel)
+    long long* fold_tl;         // diagnostics (-DRABITQ_DIAG, RABITQ_FOLD_TIMELINE): clock64 stamps of CTA 0, [16][1024]
     int fold_diag;              // diagnostics (-DRABITQ_DIAG, RABITQ_FOLD_DIAG): 1 no slow path, 2 no row ip
 };
 

@@ -82,7 +82,7 @@ def full(rep, out_md, out_json):
             tot = rd * scale.get(m["dram__bytes_read.sum"][1], 1) + wr * scale.get(m["dram__bytes_write.sum"][1], 1)
             # the bench's dominant-kernel keys: the main scan launch and the re-rank
             # scan_imma_kernel<LB, dump, retry, dense, tma-A>: the main scan has LB = dump = retry = dense = 0
-            main_scan = ("scan_imma_kernel<0, 0, 0, 0" in name) or "scan_popc" in name
+            main_scan = ("scan_imma_kernel<0, 0, 0, 0" in name) or "scan_popc" in name or "scan_fold_kernel" in name
             key = "scan" if main_scan else ("select_rerank" if "select_rerank" in name else name)
             js.setdefault(key, tot)
         except Exception:
