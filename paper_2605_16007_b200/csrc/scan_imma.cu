@@ -1318,6 +1318,7 @@ constexpr int kFxEpiW = FX_EPIW;            // epilogue warps (kFxEpiW / 4 per T
 constexpr int kFxXW = 4;                    // X producer warps (one vector row per lane)
 constexpr int kFxMmaW = 2 + kFxXW;          // warps 0 sched + B, 1 A loader, 2..5 X producers, 6 MMA
 constexpr int kFxEpi0 = kFxMmaW + 1;
+constexpr int kFxDefer = 32768;  // deferred (row, chunk) records per CTA (1 MB)
 constexpr int kFxNT = (kFxEpi0 + kFxEpiW) * 32;  // 608 threads
 constexpr int kFxCh = kFxUW / kEC;               // 8 chunks per unit and lane quarter (at most)
 constexpr uint32_t kFxBStage = kSkNG * kKC;      // 32 KB query operand
@@ -1358,6 +1359,22 @@ __device__ __forceinline__ float ipn_rows(const uint8_t* __restrict__ crow, cons
     }
     const float2 a = __half22float2(s0), b = __half22float2(s1);
     return -((a.x + a.y) + (b.x + b.y));  // -ip (the f8 accumulator's value), exact
+}
+
+// Exact keys of one vector row's flagged pairs within a 16-column chunk (one thread): the ip from the
+// e4m3 rows, the scan's estimator, one counter atomic per pair.  Called from the tail phase on the
+// deferred records (and in place when the CTA's record region is full).
+__device__ __forceinline__ void fx_row_keys(const ScanArgs& a, float2 fac, float pcf, uint32_t row, int64_t crowi,
+                                            int gcol0, uint32_t rowbits) {
+    const uint8_t* crow = a.codes8 + (size_t)crowi * a.Dp;
+    for (uint32_t m = rowbits; m; m &= m - 1) {
+        const int gcol = gcol0 + __ffs(m) - 1;
+        const ColC cq = colp_get(a.gcolp, gcol);
+        const float ipn = ipn_rows(crow, a.qbar8 + (size_t)gcol * a.Dp, a.Dp);
+        const float key = est_of<true>(__float_as_uint(ipn), cq, fac, pcf);
+        const int pos = atomicAdd(&a.cnt[cq.q], 1);
+        if (pos < a.cap) a.buf[(size_t)cq.q * a.cap + pos] = make_key(key, row);
+    }
 }
 
 // Fast pass over N 16-column chunks of a unit (one TMEM wait): the sign bits of the accumulators.
@@ -1421,6 +1438,7 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
     SkRows* urows = reinterpret_cast<SkRows*>(smem + kFxOffR);
     __shared__ int4 rec[kFxRI];
     __shared__ uint32_t next_chunk[4];
+    __shared__ uint32_t defer_n;  // flagged (row, chunk) records deferred to the tail phase
     __shared__ uint32_t mma_issued;  // tiles whose MMAs the MMA warp has issued (epilogue wait gate)
     __shared__ __align__(8) uint64_t ifull[kFxRI], iempty[kFxRI], bfull[2], bfree[2], afull[kFxSA], xfull[kFxSA],
         aempty[kFxSA], accf[2 * kFxTS], acce[kFxTS], rowf[kFxRT];
@@ -1448,6 +1466,7 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
         }
         for (int t = 0; t < kFxRT; ++t) tc::mbar_init(&rowf[t], 1);
         for (int q = 0; q < 4; ++q) next_chunk[q] = 0u;
+        defer_n = 0u;
         mma_issued = 0u;
         tc::prefetch_tmap(&tmapB);
         tc::prefetch_tmap(&tmapA);
@@ -1749,46 +1768,29 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
             __syncwarp();
             if (lane == 0) tc::mbar_arrive_s(acce_s + 8u * k);  // the slot (and its row constants) may be refilled
             if (lane == 0) FX_TL(8 + quarter, uc);
-            // ---- slow path: exact keys of the flagged pairs, chunk by chunk ----
+            // ---- flagged pairs: deferred.  Computing the exact keys here (column constants -> counter
+            // atomic -> store: three dependent global round trips) kept the warp away from its next unit
+            // for ~3 us, about one quarter-unit in six at CFG4, 1 ms of the 5.2 ms scan (RABITQ_DIAG run
+            // without the slow path).  Each flagged (row, chunk) becomes a 32-byte record in the CTA's
+            // global region (shared-memory counter, plain stores, nothing waited for); every thread of
+            // the CTA computes the keys after the last item.
             for (uint32_t f = flagged; f; f &= f - 1) {
                 const int j = __ffs(f) - 1;
-                const int cl0 = j * kEC;  // unit column of the chunk
                 const uint32_t rowbits = (uint32_t)((j < 4 ? rb0 : rb1) >> (16 * (j & 3))) & 0xFFFFu;
-                const uint32_t cols = __reduce_or_sync(0xFFFFFFFFu, rowbits);
-                // lane c < 16 owns column c: its row ballot, constants and counter atomic
-                uint32_t mybal = 0u;
-                for (uint32_t m = cols; m; m &= m - 1) {
-                    const int i2 = __ffs(m) - 1;
-                    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, (rowbits >> i2) & 1u);
-                    if (lane == i2) mybal = bal;
-                }
-                const int64_t gcol0 = (int64_t)R.z + u * wu + cl0;  // grouped row of the chunk's column 0
-                // memory-level parallelism: the column constants (owner lanes) and the code / query
-                // rows of each row's first flagged column are loaded together; the counter atomic,
-                // which needs the constants' q, is issued once they are back
-                ColC mc{};
-                int mybase = 0;
-                if (mybal) mc = colp_get(a.gcolp, (int)(gcol0 + lane));
-                const uint8_t* crow = a.codes8 + (size_t)(R.x + v) * a.Dp;
-                const int i2f = rowbits ? __ffs(rowbits) - 1 : -1;
-                float ipn0 = 0.f;
-                if (i2f >= 0) ipn0 = ipn_rows(crow, a.qbar8 + (size_t)(gcol0 + i2f) * a.Dp, a.Dp);
-                if (mybal) mybase = atomicAdd(&a.cnt[mc.q], __popc(mybal));
-                for (uint32_t m = cols; m; m &= m - 1) {
-                    const int i2 = __ffs(m) - 1;
-                    const uint32_t bal = __shfl_sync(0xFFFFFFFFu, mybal, i2);
-                    const int base = __shfl_sync(0xFFFFFFFFu, mybase, i2);
-                    ColC cq;
-                    cq.a = __shfl_sync(0xFFFFFFFFu, mc.a, i2);
-                    cq.b = __shfl_sync(0xFFFFFFFFu, mc.b, i2);
-                    cq.K = __shfl_sync(0xFFFFFFFFu, mc.K, i2);
-                    cq.nq2 = __shfl_sync(0xFFFFFFFFu, mc.nq2, i2);
-                    cq.q = __shfl_sync(0xFFFFFFFFu, mc.q, i2);
-                    if ((bal >> lane) & 1u) {
-                        const float ipn = i2 == i2f ? ipn0 : ipn_rows(crow, a.qbar8 + (size_t)(gcol0 + i2) * a.Dp, a.Dp);
-                        const float key = est_of<true>(__float_as_uint(ipn), cq, fac, pcf);
-                        const int pos = base + __popc(bal & ((1u << lane) - 1u));
-                        if (pos < a.cap) a.buf[(size_t)cq.q * a.cap + pos] = make_key(key, row);
+                const int gcol0 = (int)((int64_t)R.z + u * wu + j * kEC);  // grouped row of the chunk's column 0
+                const uint32_t has = __ballot_sync(0xFFFFFFFFu, rowbits != 0u);
+                uint32_t base = 0u;
+                if (lane == 0) base = atomicAdd(&defer_n, (uint32_t)__popc(has));
+                base = __shfl_sync(0xFFFFFFFFu, base, 0);
+                if (rowbits) {
+                    const uint32_t pos = base + (uint32_t)__popc(has & ((1u << lane) - 1u));
+                    const int64_t crowi = (int64_t)R.x + v;
+                    if (pos < (uint32_t)a.fold_defer_cap) {
+                        uint4* d = a.fold_defer + ((size_t)blockIdx.x * (size_t)a.fold_defer_cap + pos) * 2;
+                        d[0] = make_uint4(__float_as_uint(fac.x), __float_as_uint(fac.y), __float_as_uint(pcf), row);
+                        d[1] = make_uint4((uint32_t)crowi, (uint32_t)((uint64_t)crowi >> 32), (uint32_t)gcol0, rowbits);
+                    } else {
+                        fx_row_keys(a, fac, pcf, row, crowi, gcol0, rowbits);  // region full: in place
                     }
                 }
             }
@@ -1799,6 +1801,15 @@ __global__ __launch_bounds__(kFxNT, 1) void scan_fold_kernel(const __grid_consta
     __syncthreads();
     if (tid == 0) FX_CRUMB(25, 1);
     if (warp == kFxMmaW) tc::tmem_dealloc(tmem, kTmemCols);
+    {  // tail phase: the deferred records (written before the barrier above by this CTA's epilogue warps)
+        const uint32_t nd = min(defer_n, (uint32_t)a.fold_defer_cap);
+        const uint4* d = a.fold_defer + (size_t)blockIdx.x * (size_t)a.fold_defer_cap * 2;
+        for (uint32_t i = (uint32_t)tid; i < nd; i += (uint32_t)kFxNT) {
+            const uint4 w0 = d[2 * i], w1 = d[2 * i + 1];
+            fx_row_keys(a, make_float2(__uint_as_float(w0.x), __uint_as_float(w0.y)), __uint_as_float(w0.z), w0.w,
+                        (int64_t)(((uint64_t)w1.y << 32) | (uint64_t)w1.x), (int)w1.z, w1.w);
+        }
+    }
 #undef FX_CRUMB
 #undef FX_TL
 }
@@ -1997,6 +2008,11 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
                 RQ_CUDA(cudaHostGetDevicePointer(&dptr, tl_h, 0));
                 a.fold_tl = dptr;
             }
+            // deferred flagged records: kFxDefer x 32 B per CTA (a full region falls back to in-place keys)
+            WBuf<uint4> defer;
+            defer.alloc((size_t)sms * kFxDefer * 2, st);
+            a.fold_defer = defer.p;
+            a.fold_defer_cap = kFxDefer;
 #define RQ_FOLD(NK)                                                                                          \
     do {                                                                                                       \
         RQ_CUDA(cudaFuncSetAttribute(scan_fold_kernel<NK>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \

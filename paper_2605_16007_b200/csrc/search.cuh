@@ -77,6 +77,8 @@ struct ScanArgs {
     int64_t items_bound;        // upper bound on the grouping's work items (small-K item table)
     int fold;                   // 1: the small-K main scan tests survivors on the tensor cores (scan_fold_kernel)
     long long* fold_tl;         // diagnostics (-DRABITQ_DIAG, RABITQ_FOLD_TIMELINE): clock64 stamps of CTA 0, [16][1024]
+    uint4* fold_defer;          // folded scan: per-CTA regions of deferred flagged records (set by scan_imma)
+    int fold_defer_cap;         // records per CTA
     int fold_diag;              // diagnostics (-DRABITQ_DIAG, RABITQ_FOLD_DIAG): 1 no slow path, 2 no row ip
 };
 
