@@ -200,6 +200,9 @@ typedef struct {
                                                  CUDA cores (scan_small_kernel) instead of the
                                                  tensor-core folded test (scan_fold_kernel, which
                                                  runs with the nearest-list threshold only)      */
+#define RABITQ_VARIANT_FOLD_INPLACE 64u      /* folded scan: 2 deferred records per CTA instead of
+                                                 32768, so that nearly every flagged pair takes the
+                                                 region-full path (keys computed in place)        */
 
 /* Search nq queries Q [nq x d] fp32: rotate, probe the nprobe
  * nearest lists, 4-bit Philox-randomized query quantization per (q, list),

@@ -25,7 +25,7 @@ SCAN_AUTO, SCAN_POPC, SCAN_IMMA = 0, 1, 2
 RANK_EST, RANK_LOWER_BOUND = 0, 1
 # rabitq_search_opts.variant bits: alternative execution paths, identical results
 VARIANT_RADIX_PROBE, VARIANT_EXPAND_IN_KERNEL, VARIANT_NO_DENSE_RERANK, VARIANT_GENERIC_SCAN = 1, 2, 4, 8
-VARIANT_UNIFORM_SEED, VARIANT_NO_FOLD = 16, 32
+VARIANT_UNIFORM_SEED, VARIANT_NO_FOLD, VARIANT_FOLD_INPLACE = 16, 32, 64
 RERANK_FIXED, RERANK_BOUND = 0, 1
 
 

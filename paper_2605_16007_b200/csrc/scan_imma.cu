@@ -2010,9 +2010,9 @@ void scan_imma(const ScanArgs& a_in, bool lb, bool dump, bool retry, cudaStream_
             }
             // deferred flagged records: kFxDefer x 32 B per CTA (a full region falls back to in-place keys)
             WBuf<uint4> defer;
-            defer.alloc((size_t)sms * kFxDefer * 2, st);
+            a.fold_defer_cap = a_in.fold_defer_cap > 0 ? a_in.fold_defer_cap : kFxDefer;
+            defer.alloc((size_t)sms * (size_t)a.fold_defer_cap * 2, st);
             a.fold_defer = defer.p;
-            a.fold_defer_cap = kFxDefer;
 #define RQ_FOLD(NK)                                                                                          \
     do {                                                                                                       \
         RQ_CUDA(cudaFuncSetAttribute(scan_fold_kernel<NK>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \

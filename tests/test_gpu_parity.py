@@ -434,6 +434,12 @@ def test_small_scan_identical(D, N, nlist, nq):
     need = _dump_counts(idx, dmp[2], nprobe, a[2]["tau"])
     assert np.all(a[2]["survivors"] >= need), "folded test dropped a pair with est <= tau"
     assert a[2]["survivors"].sum() <= need.sum() * 1.01 + 16 * nq
+    # the folded scan defers its flagged pairs to a tail phase; with a 2-record region
+    # nearly all of them take the region-full path instead: same keys, same counts
+    fi = debug_search(idx, Q, 10, nprobe, 200, scan_path=rq.SCAN_IMMA, dump=False, variant=rq.VARIANT_FOLD_INPLACE)
+    assert np.array_equal(a[0], fi[0]) and np.array_equal(a[1], fi[1])
+    for key in ("tau", "topm_ids", "topm_est", "survivors"):
+        assert np.array_equal(a[2][key], fi[2][key]), key
     u = debug_search(idx, Q, 10, nprobe, 200, scan_path=rq.SCAN_IMMA, dump=False, variant=rq.VARIANT_UNIFORM_SEED)
     assert np.array_equal(a[0], u[0]) and np.array_equal(a[1], u[1])
     assert np.array_equal(a[2]["topm_ids"], u[2]["topm_ids"])
